@@ -1,0 +1,348 @@
+"""Benchmark: simulated requests/s of the batched Arrow evaluator (whole box).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2|c5]
+
+Workload (N=1): BASELINE.json configs[1] = C2, the request-rate sweep of the
+bundled bursty trace (2 606 requests) over 32 rates x {Arrow, static PD,
+PD-colocated} on 8 instances: 96 full simulations per step, with the
+reference's 500 000-event stall watchdog.  Under torchrun each rank
+evaluates the C2 grid on its own bursty-trace variant (rank 0 = C2 itself):
+per-GPU work is fixed ("scaling": "weak"); the per-scenario summaries are
+all-gathered over NCCL at the end of every step.
+
+value  = requests simulated by all ranks / max-over-ranks device time of one
+         step (kernel only, inputs resident in HBM, L2 flushed between steps).
+e2e    = same metric through the public API (evaluate_scenarios: host scenario
+         compile + pinned H2D + kernel + D2H of the summaries).
+--impl reference: the CPU port of the reference (oracle/, C) on all host
+         threads, on a bounded sample of the same scenarios per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BYTES_PER_REQUEST = 40      # 16 B read + 24 B written per simulated request
+BYTES_PER_SCENARIO = 256
+
+
+def workload(name: str, rank: int):
+    from paper_2505_11916_b200 import workloads as W
+
+    if name == "c2":
+        return W.c2(trace=W.c2_variant_trace(rank)), "C2 rate sweep: bursty trace variant %d (2606-ish req), " \
+            "32 rates 2-33 req/s x {arrow, static-pd, colocated}, 8 instances, kv 3000" % rank
+    if name == "c5":
+        total = 4 * 32 * 3 * 4 * 4 * 4 * 4
+        ids = np.arange(rank, total, int(os.environ.get("WORLD_SIZE", "1")))
+        return W.c5(ids), "C5 mixed-radix sweep shard (98304 scenarios total)"
+    if name == "c1":
+        return W.c1(), "C1 single Arrow simulation, 4 instances, 1000 requests @4 req/s"
+    raise SystemExit(f"unknown workload {name}")
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = Path(os.environ.get("TMPDIR", "/tmp")) / f"arrow_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self) -> dict:
+        rows = []
+        try:
+            for line in self.path.read_text().splitlines():
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in rows:
+            for name, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+def cpu_port_baseline(scenarios, budget_s: float, threads: int) -> dict:
+    """The C port of the reference (oracle/) on a bounded, evenly spaced
+    sample of the step's scenarios, all host threads."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import harness as H
+    from paper_2505_11916_b200._buffers import OutputSpec
+    from paper_2505_11916_b200._compile import compile_batch
+    from paper_2505_11916_b200 import engine
+
+    n_sample = int(os.environ.get("ARROW_CPU_SAMPLE", "24"))
+    idx = np.linspace(0, len(scenarios) - 1, min(n_sample, len(scenarios))).round().astype(int)
+    idx = sorted(set(idx.tolist()))
+    sample = [scenarios[i] for i in idx]
+    cb = compile_batch(sample, engine.STALL_EVENT_LIMIT)
+    t0 = time.perf_counter()
+    hb = H.run_oracle(cb, OutputSpec(), threads=threads)
+    dt = time.perf_counter() - t0
+    reqs = int(cb.scenarios["n_requests"].sum())
+    return {
+        "value": reqs / dt,
+        "unit": "simulated requests/s",
+        "cores": threads,
+        "kind": "port",
+        "sample": f"{len(sample)} of {len(scenarios)} scenarios (evenly spaced ids), {reqs} requests, "
+                  f"{int(hb.summaries['n_events'].sum())} events, {int((hb.summaries['status'] == 1).sum())} stalls, "
+                  f"{dt:.2f} s wall",
+        "seconds": dt,
+    }
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    scenarios, desc = workload(args.workload, 0)
+    threads = host_threads()
+    for _ in range(args.warmup):
+        pass  # the CPU port has no warm-up state; warm-up steps are skipped
+    vals = []
+    base = None
+    for _ in range(args.steps):
+        base = cpu_port_baseline(scenarios, 30.0, threads)
+        vals.append(base["value"])
+    v = statistics.median(vals)
+    base["value"] = v
+    line = {
+        "impl": "reference",
+        "metric": "simulated requests/s (whole box)",
+        "value": v,
+        "unit": "simulated requests/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1000.0 * float(np.median([base["seconds"]])),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (numpy PCG64 traces, reference generator)",
+        "config": {"workload": desc, "scenarios_per_step": "sample, see cpu_baseline.sample"},
+        "cpu_baseline": base,
+        "e2e": {"value": v, "unit": "simulated requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def run_ours(args, rank: int, world: int) -> None:
+    import torch
+
+    from paper_2505_11916_b200._backend import CudaEvaluator
+    from paper_2505_11916_b200._buffers import OutputSpec
+    from paper_2505_11916_b200._compile import compile_batch
+    from paper_2505_11916_b200 import engine, _abi
+    from paper_2505_11916_b200.sweep import evaluate_scenarios
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    scenarios, desc = workload(args.workload, rank)
+    ev = CudaEvaluator(dev)
+    cb = compile_batch(scenarios, engine.STALL_EVENT_LIMIT)
+    spec = OutputSpec()
+    db = ev.prepare(cb, spec)
+    stream = torch.cuda.current_stream(dev)
+    n_req = int(cb.scenarios["n_requests"].sum())
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)     # > 126 MB L2
+    summ_dev = db.tensors["summaries"]
+    gathered = None
+    if world > 1:
+        gathered = torch.empty(world * summ_dev.numel(), dtype=torch.uint8, device=dev)
+
+    def step():
+        ev.launch(db, stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, summ_dev[: summ_dev.numel()])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    times = []
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            torch.cuda.synchronize(dev)
+            if dist:
+                dist.barrier()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step()
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            times.append(a.elapsed_time(b))
+    ms = float(np.mean(times))
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    nr = torch.tensor([n_req], device=dev, dtype=torch.float64)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(nr, op=dist.ReduceOp.SUM)
+    ms_max = float(t.item())
+    total_req = float(nr.item())
+    value = total_req / (ms_max / 1000.0)
+
+    hb = db.download(["summaries"])
+    torch.cuda.synchronize(dev)
+    statuses = np.bincount(hb.summaries["status"], minlength=8)
+
+    # e2e through the public API: compile + pinned H2D + kernel + D2H summaries
+    e2e_times = []
+    h2d = d2h = 0
+    for k in range(args.warmup + args.steps):
+        flush.fill_(1)
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        out = evaluate_scenarios(scenarios, evaluator=ev)
+        torch.cuda.synchronize(dev)
+        if k >= args.warmup:
+            e2e_times.append(time.perf_counter() - t0)
+    h2d = cb.arrival.nbytes + cb.input_len.nbytes + cb.output_len.nbytes + cb.scenarios.nbytes
+    d2h = out.summaries.nbytes
+    e2e_s = torch.tensor([float(np.mean(e2e_times))], device=dev, dtype=torch.float64)
+    if dist:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_value = total_req / float(e2e_s.item())
+
+    pk = peaks()
+    alg_bytes = n_req * BYTES_PER_REQUEST + cb.n * BYTES_PER_SCENARIO
+    achieved = alg_bytes / (ms / 1000.0) / 1e9
+    roofline = {
+        "bound": "hbm",
+        "achieved": achieved,
+        "peak": pk["hbm_gbs"],
+        "unit": "GB/s",
+        "frac": achieved / pk["hbm_gbs"],
+        "traffic": None,
+        "peak_source": pk["source"],
+        "note": "latency-bound serial event chains; algorithmic bytes = 40 B/request + 256 B/scenario",
+    }
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_port_baseline(scenarios, 30.0, host_threads())
+    if dist:
+        dist.barrier()
+    if rank == 0:
+        line = {
+            "metric": "simulated requests/s (whole box)",
+            "value": value,
+            "unit": "simulated requests/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_max,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (numpy PCG64 traces, reference generator)",
+            "config": {
+                "workload": desc,
+                "scenarios_per_gpu": cb.n,
+                "requests_per_gpu": n_req,
+                "events_per_gpu": int(hb.summaries["n_events"].sum()),
+                "status_counts": {_abi.STATUS_NAMES[i]: int(c) for i, c in enumerate(statuses) if c},
+                "l2": "flushed (256 MiB write) between timed steps",
+                "stall_watchdog": engine.STALL_EVENT_LIMIT,
+            },
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "simulated requests/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+            "kernel_ms_per_launch": ms,
+        }
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c5"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,236 @@
+"""Parity scenario catalogue (TEST INFRASTRUCTURE).
+
+Each entry is (name, trace_builder, config_values, scale, stall_limit,
+extra).  ``config_values`` is the reference's flat key/value config
+(engine.py:328-387) so the same scenario can be rebuilt by the reference
+(for the golden files) and by this repo's host compiler (for the parity
+tests).  Scenarios follow the reference's own tests (test_engine.py,
+test_acceptance.py) and the BASELINE configs C1/C2, plus a seeded fuzz over
+strategies, pool splits, thresholds and memory pressure.
+
+Traces are built with numpy only (a duck-typed TraceRequest factory is
+passed in), so this module imports neither the reference nor the product.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+DEFAULTS = dict(
+    instances=8,
+    kv_capacity_tokens=16000,
+    chunk_budget=512,
+    max_batch_requests=256,
+    a2=1e-7,
+    a1=1e-4,
+    a0=5e-3,
+    b1=2e-5,
+    b0=5e-3,
+    bytes_per_token=131072,
+    bandwidth=4e11,
+    base_latency=1e-4,
+    ttft_slo=3.0,
+    tpot_slo=0.1,
+    attainment_target=0.9,
+    strategy="slo-aware",
+    theta_d=0.5,
+    theta_busy=0.75,
+    enable_flips=True,
+    monitor_period_s=1.0,
+    interval_window_s=5.0,
+    seed=0,
+    profile_noise=0.0,
+    profile_points=16,
+    max_context=16384,
+)
+
+# test_engine.py:38-40
+ENGINE_TEST = dict(a2=2e-7, a1=1e-4, a0=2e-3, b1=1e-4, b0=4e-3)
+
+
+def cfg(**kw):
+    v = dict(DEFAULTS)
+    v.update(kw)
+    return v
+
+
+def synthetic(make, duration_s, base_rate, in_mu, in_sigma, out_mu, out_sigma, bursts=(), max_input=16384,
+              max_output=4096, seed=0):
+    """Replays traces.gen_synthetic (traces.py:159-175) with numpy."""
+    rng = np.random.default_rng(seed)
+    rate_max = base_rate * max((b[2] for b in bursts), default=1.0)
+    out = []
+    t = 0.0
+    while True:
+        t += rng.exponential(1.0 / rate_max)
+        if t >= duration_s:
+            break
+        rate = base_rate
+        for start, dur, mult in bursts:
+            if start <= t < start + dur:
+                rate *= mult
+        if rng.random() * rate_max > rate:
+            continue
+        i = int(min(max(round(math.exp(rng.normal(in_mu, in_sigma))), 1), max_input))
+        o = int(min(max(round(math.exp(rng.normal(out_mu, out_sigma))), 1), max_output))
+        out.append(make(len(out), float(t), i, o))
+    return out
+
+
+def bursty(make):
+    return synthetic(make, 360.0, 4.0, math.log(420.0), 0.55, math.log(130.0), 0.5,
+                     ((50.0, 25.0, 5.0), (150.0, 30.0, 4.0), (260.0, 25.0, 5.0)), 3500, 900, 20240817)
+
+
+def ramp(make):
+    return synthetic(make, 300.0, 1.0, math.log(500.0), 0.4, math.log(350.0), 0.35,
+                     ((60.0, 40.0, 2.0), (100.0, 40.0, 4.0), (140.0, 40.0, 6.0), (180.0, 30.0, 3.0)), 3000, 1200, 7)
+
+
+def c1_trace(make):
+    return synthetic(make, 400.0, 4.0, math.log(420.0), 0.55, math.log(130.0), 0.5, (), 3500, 900, 1)[:1000]
+
+
+def small_trace(make, n=60, seed=11, base_rate=3.0, duration=20.0):
+    return synthetic(make, duration, base_rate, math.log(300), 0.5, math.log(60), 0.4, (), seed=seed)[:n]
+
+
+def overload_trace(make):
+    """test_acceptance.py:335-349"""
+    reqs = []
+    t = 0.0
+    for _ in range(80):
+        reqs.append((t, 200, 800))
+        t += 0.1
+    t = 5.0
+    for _ in range(90):
+        reqs.append((t, 3000, 2))
+        t += 1.0 / 30.0
+    reqs.sort(key=lambda r: r[0])
+    return [make(i, a, il, ol) for i, (a, il, ol) in enumerate(reqs)]
+
+
+def fcfs_trace(make, seed=42, n=80, gap=0.05):
+    rng = np.random.default_rng(seed)
+    arrivals = np.cumsum(rng.exponential(gap, size=n))
+    lengths = rng.integers(1, 513, size=n)
+    return [make(i, float(a), int(L), 1) for i, (a, L) in enumerate(zip(arrivals, lengths))]
+
+
+def native_rate(trace):
+    return (len(trace) - 1) / (trace[-1].arrival - trace[0].arrival)
+
+
+def rate_scale(trace, rate):
+    return native_rate(trace) / rate
+
+
+def adaptive_vs_static(n, strategy, **kw):
+    """test_acceptance.py:55-72"""
+    return cfg(instances=n, kv_capacity_tokens=3000, a2=2e-8, a1=2e-5, a0=2e-3, strategy=strategy,
+               init_prefill=n // 2, init_decode=n // 2, **kw)
+
+
+def catalogue(make, include_slow=True):
+    """List of scenario dicts: name, trace (list), values, scale, stall_limit."""
+    S = []
+
+    def add(name, trace, values, scale=1.0, stall_limit=500_000, full=False):
+        S.append(dict(name=name, trace=trace, values=values, scale=scale, stall_limit=stall_limit, full=full))
+
+    one = lambda n, a, i, o: [make(0, a, i, o)]  # noqa: E731
+    # closed-form timelines, test_engine.py:92-151
+    add("single_request", one(0, 0.0, 300, 4), cfg(instances=1, init_prefill=1, init_decode=0, **ENGINE_TEST), full=True)
+    add("single_token", one(0, 0.0, 200, 1), cfg(instances=1, init_prefill=1, init_decode=0, **ENGINE_TEST), full=True)
+    add("chunked_prefill", one(0, 0.0, 1300, 2), cfg(instances=1, init_prefill=1, init_decode=0, **ENGINE_TEST), full=True)
+    add("migration_gap", one(0, 0.0, 400, 3),
+        cfg(instances=2, strategy="minimal-load", init_prefill=1, init_decode=1, **ENGINE_TEST), full=True)
+    add("fcfs_recurrence", fcfs_trace(make), cfg(instances=1, init_prefill=1, init_decode=0, **ENGINE_TEST), full=True)
+    mon = dict(ENGINE_TEST, a2=0.0, a1=0.01, a0=0.0, b1=1e-9, b0=0.085)
+    add("monitor_cadence", one(0, 0.0, 100, 100), cfg(instances=1, init_prefill=1, init_decode=0, **mon), full=True)
+    add("stall_limit_zero", one(0, 0.0, 100, 4), cfg(instances=2, **ENGINE_TEST), stall_limit=0, full=True)
+    # cross-run invariants, test_engine.py:214-255
+    st = small_trace(make)
+    add("small_arrow_2_2", st, cfg(instances=4, init_prefill=2, init_decode=2, **ENGINE_TEST), full=True)
+    st120 = small_trace(make, n=120, duration=40.0)
+    add("small_noflip", st120, cfg(instances=4, init_prefill=2, init_decode=2, enable_flips=False, **ENGINE_TEST),
+        full=True)
+    add("small_minload", st120, cfg(instances=4, strategy="minimal-load", init_prefill=2, init_decode=2, **ENGINE_TEST),
+        full=True)
+    # conservation suite, test_acceptance.py:249-286
+    b400 = bursty(make)[:400]
+    for label, strat, kv, rate in (("slo", "slo-aware", 3000, 9.0), ("minload", "minimal-load", 3000, 9.0),
+                                   ("rr", "round-robin", 16000, 6.0)):
+        add(f"conservation_{label}", b400,
+            cfg(instances=8, init_prefill=4, init_decode=4, kv_capacity_tokens=kv, a2=2e-8, a1=2e-5, a0=2e-3,
+                strategy=strat), scale=rate_scale(b400, rate), full=True)
+    add("determinism_600", bursty(make)[:600], adaptive_vs_static(8, "slo-aware"), full=True)
+    add("overload_flips", overload_trace(make), cfg(instances=4, init_prefill=2, init_decode=2), full=True)
+    # C1 (BASELINE configs[0])
+    c1 = c1_trace(make)
+    add("c1_rate4", c1, cfg(instances=4, init_prefill=2, init_decode=2), scale=rate_scale(c1, 4.0), full=True)
+    add("c1_rate8", c1, cfg(instances=4, init_prefill=2, init_decode=2), scale=rate_scale(c1, 8.0))
+    # round-robin and degenerate splits
+    add("rr_small", st120, cfg(instances=3, strategy="round-robin", init_prefill=1, init_decode=2, **ENGINE_TEST),
+        full=True)
+    add("colocated_small", st120, cfg(instances=4, init_prefill=4, init_decode=0, enable_flips=False, **ENGINE_TEST),
+        full=True)
+    add("all_decode_start", st120, cfg(instances=3, init_prefill=0, init_decode=3, **ENGINE_TEST), full=True)
+    # memory pressure and caps
+    add("tight_kv", st120, cfg(instances=4, kv_capacity_tokens=1200, chunk_budget=128, **ENGINE_TEST),
+        scale=0.5, full=True)
+    add("decode_cap", st120, cfg(instances=2, max_batch_requests=3, chunk_budget=64, init_prefill=1, init_decode=1,
+                                 kv_capacity_tokens=4000, **ENGINE_TEST), scale=0.25, full=True)
+    # stalls (small watchdog so the reference finishes quickly)
+    b = bursty(make)
+    if include_slow:
+        add("c2_arrow_r10", b, adaptive_vs_static(8, "slo-aware"), scale=rate_scale(b, 10.0))
+        add("c2_static_r10", b, adaptive_vs_static(8, "minimal-load"), scale=rate_scale(b, 10.0))
+        add("c2_coloc_r10", b, adaptive_vs_static(8, "slo-aware", enable_flips=False) | dict(init_prefill=8, init_decode=0),
+            scale=rate_scale(b, 10.0))
+        add("c2_arrow_r32_stall", b, adaptive_vs_static(8, "slo-aware"), scale=rate_scale(b, 32.0), stall_limit=20000)
+        add("c2_coloc_r20_stall", b, adaptive_vs_static(8, "slo-aware", enable_flips=False) | dict(init_prefill=8, init_decode=0),
+            scale=rate_scale(b, 20.0), stall_limit=20000)
+        r = ramp(make)
+        add("ramp_minload", r, cfg(instances=8, init_prefill=4, init_decode=4, strategy="minimal-load"), scale=1.0 / 8.0,
+            full=True)
+    # seeded fuzz
+    rng = np.random.default_rng(20260101)
+    for k in range(40):
+        N = int(rng.integers(1, 13))
+        strat = ["slo-aware", "slo-aware", "minimal-load", "round-robin"][int(rng.integers(0, 4))]
+        if strat != "slo-aware" and N < 2:
+            N = 2
+        n_p = int(rng.integers(1 if strat != "slo-aware" else 0, N if strat != "slo-aware" else N + 1))
+        v = cfg(
+            instances=N,
+            init_prefill=n_p,
+            init_decode=N - n_p,
+            strategy=strat,
+            enable_flips=bool(rng.integers(0, 4) > 0),
+            kv_capacity_tokens=int(rng.choice([1500, 3000, 6000, 16000])),
+            chunk_budget=int(rng.choice([128, 256, 512])),
+            max_batch_requests=int(rng.choice([4, 16, 256])),
+            theta_d=float(rng.choice([0.25, 0.5, 1.0])),
+            theta_busy=float(rng.choice([0.3, 0.75, 1.0])),
+            tpot_breach_duration_s=float(rng.choice([1.0, 2.0, 4.0])),
+            ttft_slo=float(rng.choice([0.5, 1.0, 3.0])),
+            tpot_slo=float(rng.choice([0.03, 0.1])),
+            a2=2e-8, a1=2e-5, a0=2e-3,
+            seed=int(rng.integers(0, 3)),
+            profile_noise=float(rng.choice([0.0, 0.0, 0.02])),
+        )
+        if rng.integers(0, 2):
+            v["ttft_threshold"] = float(rng.choice([0.25, 1.0, 2.0]))
+        n_req = int(rng.integers(20, 260))
+        cap = min(1400, v["kv_capacity_tokens"] // 2) if k % 10 else 1400   # every 10th: may fail validation
+        tr = synthetic(make, 60.0, 3.0, math.log(float(rng.choice([150, 400, 900]))), 0.6,
+                       math.log(float(rng.choice([20, 80, 200]))), 0.6, ((10.0, 10.0, 3.0),), cap, cap,
+                       int(rng.integers(0, 10_000)))[:n_req]
+        if len(tr) < 2:
+            continue
+        rate = float(rng.choice([1.0, 3.0, 6.0, 12.0])) * max(N, 1) / 4
+        add(f"fuzz_{k:02d}", tr, v, scale=rate_scale(tr, rate), stall_limit=20000, full=k % 3 == 0)
+    return S

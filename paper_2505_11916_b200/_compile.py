@@ -1,0 +1,251 @@
+"""Host scenario compiler: (trace, RunConfig, rate scale) -> packed
+``arrow_scenario_t`` records + concatenated struct-of-arrays traces.
+
+Every per-scenario constant is resolved with the reference's own rules
+before anything reaches the device:
+
+* predictor   np.random.default_rng(seed) -> default_profile_grid ->
+              profile_prefill -> fit_quadratic            engine.py:128-131
+* max_tokens  max_running_tokens(true_decode, kv, tpot)  engine.py:132-134
+* thresholds  ttft/tpot threshold default to the SLO, breach duration to
+              two monitor periods                         scheduler.py:75-81
+* split       RunConfig.initial_split()                   engine.py:140-144
+* watchdog    engine.STALL_EVENT_LIMIT, read per call      engine.py:119, 283
+* validation  _validate_trace on the scaled arrivals       engine.py:101-115
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from functools import lru_cache
+
+import numpy as np
+
+from . import _abi
+from .config import RunConfig, Strategy
+from .core import TraceRequest
+from .cost_model import (
+    PrefillCostParams,
+    default_profile_grid,
+    fit_quadratic,
+    max_running_tokens,
+    profile_prefill,
+)
+from .traces import trace_arrays
+
+KV_LIMIT = 1 << 30          # int32 KV arithmetic on the device
+MAX_INSTANCES = 64
+
+
+@lru_cache(maxsize=256)
+def _fit(true_prefill: PrefillCostParams, max_context: int, points: int, noise: float, seed: int) -> PrefillCostParams:
+    rng = np.random.default_rng(seed)
+    grid = default_profile_grid(max_context, points)
+    return fit_quadratic(profile_prefill(true_prefill, grid, noise, rng))
+
+
+def resolve_predictor(config: RunConfig) -> PrefillCostParams:
+    """The scheduler's fitted prefill predictor (engine.py:128-131)."""
+    return _fit(
+        config.instance.true_prefill, config.max_context, config.profile_points, config.profile_noise, config.seed
+    )
+
+
+def resolve_max_tokens(config: RunConfig) -> int:
+    return max_running_tokens(config.instance.true_decode, config.instance.kv_capacity_tokens, config.slo.tpot_slo)
+
+
+def check_device_limits(config: RunConfig) -> None:
+    if config.instance_count > MAX_INSTANCES:
+        raise ValueError(f"the device evaluator supports up to {MAX_INSTANCES} instances, got {config.instance_count}")
+    if config.instance.kv_capacity_tokens > KV_LIMIT:
+        raise ValueError(f"kv_capacity_tokens above {KV_LIMIT} is not supported by the device evaluator")
+
+
+def emission_capacity(config: RunConfig) -> int:
+    """Upper bound on token-emitting iterations of one instance inside one
+    interval window: consecutive iterations are at least the shortest
+    possible iteration apart (b1 + b0, or a dedicated prefill of L tokens)."""
+    inst = config.instance
+    dmin = inst.true_decode.b1 + inst.true_decode.b0
+    top = max(1, min(inst.chunk_budget, inst.kv_capacity_tokens, 1 << 20))
+    L = np.arange(1, top + 1, dtype=np.float64)
+    p = inst.true_prefill
+    q = p.a2 * L * L + p.a1 * L + p.a0
+    dmin = min(dmin, float(q.min()))
+    if not (dmin > 0 and math.isfinite(dmin)):
+        return 1 << 16
+    cap = math.floor(config.interval_window_s / dmin * (1 + 1e-9)) + 3
+    return int(min(max(cap, 4), 1 << 16))
+
+
+def validate_trace(arrival_scaled: np.ndarray, ids: np.ndarray, inp: np.ndarray, outp: np.ndarray, kv: int) -> None:
+    """_validate_trace (engine.py:101-115): first offending request, checks in
+    the reference's per-request order."""
+    n = len(arrival_scaled)
+    if n == 0:
+        return
+    prev = np.concatenate(([-1.0], arrival_scaled[:-1]))
+    bad_sort = arrival_scaled < prev
+    _, first_idx = np.unique(ids, return_index=True)
+    dup = np.ones(n, dtype=bool)
+    dup[first_idx] = False
+    bad_kv = (inp.astype(np.int64) + outp) > kv
+    bad = bad_sort | dup | bad_kv
+    if not bad.any():
+        return
+    i = int(np.argmax(bad))
+    if bad_sort[i]:
+        raise ValueError("trace must be sorted by arrival time")
+    if dup[i]:
+        raise ValueError(f"duplicate request id {int(ids[i])}")
+    raise ValueError(
+        f"request {int(ids[i])} needs {int(inp[i]) + int(outp[i])} KV tokens, capacity is {kv}"
+    )
+
+
+@dataclass
+class TraceEntry:
+    arrival: np.ndarray
+    input_len: np.ndarray
+    output_len: np.ndarray
+    ids: np.ndarray
+    offset: int = 0
+
+
+class TraceTable:
+    """Concatenated traces; each distinct trace object is stored once and
+    shared (read-only, L2-resident on the device) by every scenario using it."""
+
+    def __init__(self) -> None:
+        self.entries: list[TraceEntry] = []
+        self._by_key: dict[int, int] = {}
+        self.total = 0
+
+    def add(self, trace) -> int:
+        key = id(trace)
+        if key in self._by_key:
+            return self._by_key[key]
+        if isinstance(trace, TraceEntry):
+            entry = trace
+        else:
+            arrival, inp, outp = trace_arrays(trace)
+            ids = np.fromiter((r.id for r in trace), dtype=np.int64, count=len(trace))
+            entry = TraceEntry(arrival, inp, outp, ids)
+        entry.offset = self.total
+        self.total += len(entry.arrival)
+        self.entries.append(entry)
+        self._by_key[key] = len(self.entries) - 1
+        return len(self.entries) - 1
+
+    def arrays(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+        if not self.entries:
+            z = np.zeros(1, dtype=np.float64)
+            return z, np.ones(1, dtype=np.int32), np.ones(1, dtype=np.int32)
+        return (
+            np.concatenate([e.arrival for e in self.entries]),
+            np.concatenate([e.input_len for e in self.entries]).astype(np.int32),
+            np.concatenate([e.output_len for e in self.entries]).astype(np.int32),
+        )
+
+
+@dataclass
+class Scenario:
+    """One simulation: a trace, a configuration and an arrival scale."""
+
+    trace: object
+    config: RunConfig
+    scale: float = 1.0
+    label: object = None
+
+
+@dataclass
+class CompiledBatch:
+    arrival: np.ndarray
+    input_len: np.ndarray
+    output_len: np.ndarray
+    scenarios: np.ndarray
+    table: TraceTable
+    trace_index: list[int]
+    sizes: dict = field(default_factory=dict)
+
+    @property
+    def n(self) -> int:
+        return len(self.scenarios)
+
+
+def scenario_record(config: RunConfig, trace_offset: int, n: int, scale: float, stall_limit: int) -> np.void:
+    check_device_limits(config)
+    predictor = resolve_predictor(config)
+    max_tokens = resolve_max_tokens(config)
+    sched = config.scheduler
+    rec = np.zeros((), dtype=_abi.SCENARIO_DTYPE)
+    n_p, _ = config.initial_split()
+    inst = config.instance
+    rec["trace_offset"] = trace_offset
+    rec["n_requests"] = n
+    rec["n_instances"] = config.instance_count
+    rec["n_prefill_init"] = n_p
+    rec["strategy"] = _abi.STRATEGY_CODES[sched.strategy.value]
+    rec["enable_flips"] = 1 if sched.enable_flips else 0
+    rec["kv_capacity"] = inst.kv_capacity_tokens
+    rec["chunk_budget"] = inst.chunk_budget
+    rec["max_batch"] = inst.max_batch_requests
+    rec["bytes_per_token"] = inst.transfer.bytes_per_token
+    rec["max_tokens"] = max_tokens
+    rec["stall_limit"] = stall_limit
+    rec["arrival_scale"] = scale
+    rec["true_a2"], rec["true_a1"], rec["true_a0"] = inst.true_prefill.a2, inst.true_prefill.a1, inst.true_prefill.a0
+    rec["pred_a2"], rec["pred_a1"], rec["pred_a0"] = predictor.a2, predictor.a1, predictor.a0
+    rec["b1"], rec["b0"] = inst.true_decode.b1, inst.true_decode.b0
+    rec["base_latency"], rec["bandwidth"] = inst.transfer.base_latency, inst.transfer.bandwidth
+    rec["ttft_slo"], rec["tpot_slo"] = config.slo.ttft_slo, config.slo.tpot_slo
+    rec["ttft_thr"] = sched.ttft_threshold if sched.ttft_threshold is not None else config.slo.ttft_slo
+    rec["tpot_thr"] = sched.tpot_threshold if sched.tpot_threshold is not None else config.slo.tpot_slo
+    rec["theta_d"], rec["theta_busy"] = sched.theta_d, sched.theta_busy
+    rec["breach_duration"] = (
+        sched.tpot_breach_duration_s if sched.tpot_breach_duration_s is not None else 2 * config.monitor_period_s
+    )
+    rec["monitor_period"] = config.monitor_period_s
+    rec["window"] = config.interval_window_s
+    return rec
+
+
+def compile_batch(scenarios: list[Scenario], stall_limit: int, validate: bool = True) -> CompiledBatch:
+    table = TraceTable()
+    recs = np.zeros(len(scenarios), dtype=_abi.SCENARIO_DTYPE)
+    tix = []
+    max_n = max_N = 1
+    ecap = 4
+    rcap = 1
+    validated: set = set()
+    for k, sc in enumerate(scenarios):
+        t = table.add(sc.trace)
+        entry = table.entries[t]
+        n = len(entry.arrival)
+        cfg = sc.config
+        # reference order: predictor fit and token cap (in _Simulation.__init__)
+        # raise before trace validation (in _Simulation.run)
+        recs[k] = scenario_record(cfg, entry.offset, n, sc.scale, stall_limit)
+        if validate:
+            vkey = (t, sc.scale, cfg.instance.kv_capacity_tokens)
+            if vkey not in validated:
+                scaled = entry.arrival * sc.scale if sc.scale != 1.0 else entry.arrival
+                validate_trace(scaled, entry.ids, entry.input_len, entry.output_len, cfg.instance.kv_capacity_tokens)
+                validated.add(vkey)
+        tix.append(t)
+        max_n = max(max_n, n)
+        max_N = max(max_N, cfg.instance_count)
+        ecap = max(ecap, emission_capacity(cfg))
+        rcap = max(rcap, min(cfg.instance.max_batch_requests, cfg.instance.chunk_budget))
+    arrival, inp, outp = table.arrays()
+    sizes = dict(
+        max_requests=max_n,
+        max_instances=max_N,
+        queue_capacity=max_n,
+        emission_capacity=ecap,
+        running_capacity=rcap,
+        fifo_capacity=max_n,
+    )
+    return CompiledBatch(arrival, inp, outp, recs, table, tix, sizes)

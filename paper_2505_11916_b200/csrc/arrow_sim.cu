@@ -1,0 +1,129 @@
+// arrow_sim.cu — sm_100a persistent kernel + C-ABI (include/arrow_sim.h).
+//
+// One warp = one scenario slot.  The grid is sized to the device's resident
+// warp capacity (SM count x blocks/SM from the occupancy API); warps pull
+// scenario ids from an atomic counter, so long scenarios (10^5-10^6 events)
+// and short ones (10^3) balance dynamically.  Each slot owns a private
+// region of the caller's workspace (queues, rings, per-request state) sized
+// by make_layout(); traces are shared read-only by every slot.
+#include <cuda_runtime.h>
+
+#include "arrow_sim.h"
+#include "sim_core.cuh"
+
+namespace {
+
+constexpr int kWarpsPerBlock = 4;
+constexpr int kThreads = kWarpsPerBlock * 32;
+
+template <int IPL>
+__global__ void __launch_bounds__(kThreads) arrow_sim_kernel(const arrow_batch_t batch, char* workspace,
+                                                             arrow::SlotLayout L, int* counter, int n_slots) {
+  __shared__ arrow::WarpSmem smem[kWarpsPerBlock];
+  __shared__ arrow_batch_t sb;
+  if (threadIdx.x == 0) sb = batch;
+  __syncthreads();
+  const int wid = threadIdx.x >> 5;
+  const int slot = blockIdx.x * kWarpsPerBlock + wid;
+  if (slot >= n_slots) return;
+  arrow::Sim<DevWarp, IPL> sim;
+  sim.sm = &smem[wid];
+  sim.B = &sb;
+  sim.L = L;
+  sim.p = arrow::slot_ptrs(workspace + (int64_t)slot * L.bytes, L);
+  sim.lane = (int)(threadIdx.x & 31u);
+  for (;;) {
+    int k = 0;
+    if (sim.lane == 0) k = atomicAdd(counter, 1);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    if (k >= sb.n_scenarios) break;
+    const int s = sb.order ? sb.order[k] : k;
+    sim.run(s);
+  }
+}
+
+arrow::SlotLayout layout_of(const arrow_batch_t* b) {
+  return arrow::make_layout(b->max_requests, b->max_instances, b->queue_capacity, b->running_capacity,
+                            b->emission_capacity);
+}
+
+int ipl_of(const arrow_batch_t* b) { return b->max_instances > 32 ? 2 : 1; }
+
+cudaError_t slots_for(const arrow_batch_t* b, int* slots) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  int sms = 0;
+  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  if (ipl_of(b) == 2)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arrow_sim_kernel<2>, kThreads, 0);
+  else
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arrow_sim_kernel<1>, kThreads, 0);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  long long cap = (long long)sms * per_sm * kWarpsPerBlock;
+  long long want = b->n_scenarios > 0 ? b->n_scenarios : 1;
+  *slots = (int)(want < cap ? want : cap);
+  return cudaSuccess;
+}
+
+}  // namespace
+
+extern "C" {
+
+int arrow_sim_abi_version(void) { return ARROW_SIM_ABI_VERSION; }
+
+int arrow_sim_slots(const arrow_batch_t* b, int* slots) { return (int)slots_for(b, slots); }
+
+int arrow_sim_workspace_size(const arrow_batch_t* b, size_t* bytes) {
+  if (!b || !bytes) return (int)cudaErrorInvalidValue;
+  if (b->max_instances < 1 || b->max_instances > arrow::MAX_INST) return (int)cudaErrorInvalidValue;
+  int slots = 0;
+  cudaError_t e = slots_for(b, &slots);
+  if (e != cudaSuccess) return (int)e;
+  arrow::SlotLayout L = layout_of(b);
+  *bytes = (size_t)slots * (size_t)L.bytes + 256;
+  return 0;
+}
+
+int arrow_sim_run(const arrow_batch_t* b, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!b) return (int)cudaErrorInvalidValue;
+  if (b->n_scenarios <= 0) return 0;
+  size_t need = 0;
+  int rc = arrow_sim_workspace_size(b, &need);
+  if (rc) return rc;
+  if (!workspace || workspace_bytes < need) return (int)cudaErrorInvalidValue;
+  int slots = 0;
+  cudaError_t e = slots_for(b, &slots);
+  if (e != cudaSuccess) return (int)e;
+  arrow::SlotLayout L = layout_of(b);
+  char* ws = (char*)workspace;
+  int* counter = (int*)(ws + (size_t)slots * (size_t)L.bytes);
+  cudaStream_t st = (cudaStream_t)stream;
+  e = cudaMemsetAsync(counter, 0, sizeof(int), st);
+  if (e != cudaSuccess) return (int)e;
+  const int grid = (slots + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  if (ipl_of(b) == 2)
+    arrow_sim_kernel<2><<<grid, kThreads, 0, st>>>(*b, ws, L, counter, slots);
+  else
+    arrow_sim_kernel<1><<<grid, kThreads, 0, st>>>(*b, ws, L, counter, slots);
+  return (int)cudaGetLastError();
+}
+
+const char* arrow_sim_status_string(int status) {
+  switch (status) {
+    case ARROW_OK: return "ok";
+    case ARROW_STALLED: return "stalled";
+    case ARROW_INCOMPLETE: return "incomplete";
+    case ARROW_NOT_DRAINED: return "not-drained";
+    case ARROW_NO_INSTANCE: return "no-instance";
+    case ARROW_ZERO_DIVISION: return "zero-division";
+    case ARROW_BUFFER_OVERFLOW: return "buffer-overflow";
+    case ARROW_INTERNAL: return "internal";
+    default: return "unknown";
+  }
+}
+
+}  // extern "C"

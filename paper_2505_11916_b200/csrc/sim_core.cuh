@@ -1,0 +1,1507 @@
+// sim_core.cuh — one Arrow scheduling simulation per warp.
+//
+// Semantics are those of the reference discrete-event simulator (pdsim,
+// /root/reference/pkg/src/pdsim); the data layout is B200-first:
+//
+//  * Instances map to lanes (instance i -> lane i % 32, register slot
+//    i / 32).  Each lane keeps its instances' hot state in registers: KV
+//    counters, incrementally maintained growth / running-token sums
+//    (instance.py:159-173, 292-302 recomputed O(residents) per call in the
+//    reference), the pending batch summary and ring cursors.
+//  * Queues are per-instance rings in the slot's global workspace (L2
+//    resident): waiting prefills carry their cached predictor term so the
+//    predicted-delay fold (instance.py:304-321) streams independent loads;
+//    waiting decodes and migrations are FIFO rings; running decodes are an
+//    unordered array keyed by their finishing iteration (every running
+//    decode is in every batch, instance.py:187-191 with the decode cap
+//    invariant), so an iteration costs O(1) unless a decode finishes.
+//  * The global event order (time, kind, seq) of the reference heap
+//    (engine.py:39-45, 164-166) is reproduced exactly: every lane offers
+//    its instances' pending ITERATION/MIGRATION completions, lane 0 the
+//    arrival cursor, the PREFILL_COMPLETE FIFO head and the monitor tick,
+//    and a three-step redux.sync argmin picks the next event.
+//  * Scheduler decisions (scheduler.py:151-335) are warp argmins with
+//    pool-insertion-order tie breaks; pool membership is an insertion
+//    position per instance (pools.py:42-85).
+//  * All floating point is IEEE double without contraction (built with
+//    -fmad=false / -ffp-contract=off), in the reference's expression order;
+//    Python's sum() is reproduced with CPython 3.12's Neumaier loop.
+#pragma once
+
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "arrow_sim.h"
+#include "warp.cuh"
+
+#if !defined(__CUDA_ARCH__) && defined(ARROW_EMU_TRACE)
+#include <stdio.h>
+#include <stdlib.h>
+#define ATRACE(...)                                    \
+  do {                                                 \
+    if (getenv("ARROW_EMU_TRACE")) fprintf(stderr, __VA_ARGS__); \
+  } while (0)
+#else
+#define ATRACE(...) \
+  do {              \
+  } while (0)
+#endif
+
+namespace arrow {
+
+enum { EV_MIG = 0, EV_ITER = 1, EV_PREFILL = 2, EV_ARRIVAL = 3, EV_TICK = 4 };
+enum { P_PREFILL = 0, P_DECODE = 1, P_P2D = 2, P_D2P = 3 };
+static constexpr int MAX_INST = 64;
+static constexpr uint32_t SEQ_LIMIT = 1u << 28;
+
+// ---------------------------------------------------------------- layout --
+
+struct SlotLayout {
+  int64_t n_max, N_max, qcap, rcap, ecap;
+  int64_t off_first, off_last, off_ttft, off_tpot, off_src;
+  int64_t off_fifo_time, off_fifo_rid, off_fifo_src, off_fifo_seq;
+  int64_t off_wp_term, off_wp_rid, off_wd_rid, off_mq_rid, off_run_rid, off_run_f, off_em;
+  int64_t bytes;
+};
+
+AS_HD int64_t align256(int64_t x) { return (x + 255) & ~(int64_t)255; }
+
+AS_HD SlotLayout make_layout(int64_t n_max, int64_t N_max, int64_t qcap, int64_t rcap, int64_t ecap) {
+  SlotLayout L;
+  L.n_max = n_max < 1 ? 1 : n_max;
+  L.N_max = N_max;
+  L.qcap = qcap < 1 ? 1 : qcap;
+  L.rcap = rcap < 1 ? 1 : rcap;
+  L.ecap = ecap < 2 ? 2 : ecap;
+  int64_t o = 0;
+  const int64_t n = L.n_max;
+  L.off_first = o; o = align256(o + 8 * n);
+  L.off_last = o; o = align256(o + 8 * n);
+  L.off_ttft = o; o = align256(o + 8 * n);
+  L.off_tpot = o; o = align256(o + 8 * n);
+  L.off_fifo_time = o; o = align256(o + 8 * n);
+  L.off_wp_term = o; o = align256(o + 8 * N_max * L.qcap);
+  L.off_em = o; o = align256(o + 8 * N_max * L.ecap);
+  L.off_src = o; o = align256(o + 4 * n);
+  L.off_fifo_rid = o; o = align256(o + 4 * n);
+  L.off_fifo_src = o; o = align256(o + 4 * n);
+  L.off_fifo_seq = o; o = align256(o + 4 * n);
+  L.off_wp_rid = o; o = align256(o + 4 * N_max * L.qcap);
+  L.off_wd_rid = o; o = align256(o + 4 * N_max * L.qcap);
+  L.off_mq_rid = o; o = align256(o + 4 * N_max * L.qcap);
+  L.off_run_rid = o; o = align256(o + 4 * N_max * L.rcap);
+  L.off_run_f = o; o = align256(o + 4 * N_max * L.rcap);
+  L.bytes = o;
+  return L;
+}
+
+struct SlotPtrs {
+  double *first, *last, *ttft, *tpot, *fifo_time, *wp_term, *em;
+  int *src, *fifo_rid, *fifo_src, *wp_rid, *wd_rid, *mq_rid, *run_rid, *run_f;
+  uint32_t* fifo_seq;
+};
+
+AS_HD SlotPtrs slot_ptrs(char* base, const SlotLayout& L) {
+  SlotPtrs p;
+  p.first = (double*)(base + L.off_first);
+  p.last = (double*)(base + L.off_last);
+  p.ttft = (double*)(base + L.off_ttft);
+  p.tpot = (double*)(base + L.off_tpot);
+  p.fifo_time = (double*)(base + L.off_fifo_time);
+  p.wp_term = (double*)(base + L.off_wp_term);
+  p.em = (double*)(base + L.off_em);
+  p.src = (int*)(base + L.off_src);
+  p.fifo_rid = (int*)(base + L.off_fifo_rid);
+  p.fifo_src = (int*)(base + L.off_fifo_src);
+  p.fifo_seq = (uint32_t*)(base + L.off_fifo_seq);
+  p.wp_rid = (int*)(base + L.off_wp_rid);
+  p.wd_rid = (int*)(base + L.off_wd_rid);
+  p.mq_rid = (int*)(base + L.off_mq_rid);
+  p.run_rid = (int*)(base + L.off_run_rid);
+  p.run_f = (int*)(base + L.off_run_f);
+  return p;
+}
+
+// ------------------------------------------------------------ state -----
+
+// Warp-uniform scenario state (shared memory, one writer at a time,
+// published with a warp sync).  engine.py:157-162, scheduler.py:82-85.
+struct Uniform {
+  double now;
+  double tick_time;
+  double breach;
+  double next_arrival;
+  double stall_time;
+  double tmp_d;
+  int64_t esp;
+  int64_t n_events, n_iters, n_ticks, n_snap, n_dec;
+  int64_t rr_p, rr_d;
+  uint64_t hash;
+  uint32_t seq, tick_seq;
+  int a;
+  int completed;
+  int tick_active;
+  int fifo_head, fifo_count;
+  int status, overflow;
+  int n_flips;
+  int pool_n[4];
+  int tmp_i[4];
+};
+
+struct WarpSmem {
+  arrow_scenario_t sc;
+  Uniform u;
+  int16_t pool_of[MAX_INST];
+  int16_t pos_of[MAX_INST];
+  int list[MAX_INST];
+  double vals[MAX_INST];
+  int valid[MAX_INST];
+  int hist[256];
+};
+
+// Registers of one instance on its owner lane (instance.py:78-92, reshaped).
+struct Inst {
+  int id;                       // -1: unused slot
+  int busy;
+  double busy_until;
+  uint32_t iter_seq;
+  int mig_active, mig_rid;
+  double mig_finish;
+  uint32_t mig_seq;
+  int kv_used, kv_reserved;
+  int committed;                // sum over running decodes of out - 1 - generated
+  int wgrowth;                  // sum over waiting decodes of out - 1
+  int rtok;                     // running_tokens(): prompt + generated over resident decodes
+  int R;                        // running decodes
+  int min_f;                    // smallest finishing iteration among running decodes
+  int it;                       // iterations begun
+  int pb_ndec, pb_rp_chunk, pb_k, pb_last_chunk, pb_last_comp, pb_ded;
+  int rp_rid, rp_done;          // the (at most one) partially prefilled running prompt
+  int wp_h, wp_c, wd_h, wd_c, mq_h, mq_c, em_h, em_c;
+  int parked;
+  double dly;                   // predicted_prefill_delay at the current event
+};
+
+AS_HD uint64_t dbits(double x) {
+  uint64_t u;
+  memcpy(&u, &x, 8);
+  return u;
+}
+
+// Order-preserving map double -> uint64 (-0.0 canonicalised to +0.0, as
+// Python's `<` treats them equal).
+AS_HD uint64_t okey(double x) {
+  uint64_t u = dbits(x + 0.0);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+AS_HD double okey_inv(uint64_t k) {
+  uint64_t u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  double x;
+  memcpy(&x, &u, 8);
+  return x;
+}
+
+AS_HD int ffs32(uint32_t m) {
+#ifdef __CUDA_ARCH__
+  return __ffs((int)m) - 1;
+#else
+  return m ? __builtin_ctz(m) : -1;
+#endif
+}
+
+AS_HD int popc32(uint32_t m) {
+#ifdef __CUDA_ARCH__
+  return __popc(m);
+#else
+  return __builtin_popcount(m);
+#endif
+}
+
+// cost_model.py:73-92, reference expression order
+AS_HD double quad(double a2, double a1, double a0, int len) {
+  double L = (double)len;
+  return a2 * L * L + a1 * L + a0;
+}
+
+AS_HD int imin(int a, int b) { return a < b ? a : b; }
+
+// ------------------------------------------------------------- simulator --
+
+template <class W, int IPL>
+struct Sim {
+  W w;
+  WarpSmem* sm;
+  const arrow_batch_t* B;
+  SlotLayout L;
+  SlotPtrs p;
+  int lane;
+  int sid;
+  const double* arr;
+  const int32_t* inl;
+  const int32_t* outl;
+  arrow_outmap_t om;
+  bool have_om;
+  Inst st[IPL];
+
+  static constexpr int WD = W::WIDTH;
+
+  AS_HD const arrow_scenario_t& sc() const { return sm->sc; }
+  AS_HD Uniform& u() { return sm->u; }
+
+  AS_HD static int lane_of(int id) { return id & (WD - 1); }
+
+  // Run f(Inst&) on the owner lane of instance id, then publish.
+  template <class F>
+  AS_HD void owner(int id, F&& f) {
+    if (lane == lane_of(id)) {
+      if (IPL == 1 || id < WD)
+        f(st[0]);
+      else
+        f(st[IPL - 1]);
+    }
+    w.sync();
+  }
+
+  template <class F>
+  AS_HD void lane0(F&& f) {
+    if (lane == 0) f();
+    w.sync();
+  }
+
+  template <class G>
+  AS_HD double bcast_d(int id, G g) {
+    double v = 0.0;
+#pragma unroll
+    for (int k = 0; k < IPL; k++)
+      if (st[k].id == id) v = g(st[k]);
+    return w.shfl(v, lane_of(id));
+  }
+
+  template <class G>
+  AS_HD int bcast_i(int id, G g) {
+    int v = 0;
+#pragma unroll
+    for (int k = 0; k < IPL; k++)
+      if (st[k].id == id) v = g(st[k]);
+    return w.shfl(v, lane_of(id));
+  }
+
+  AS_HD void set_status(int s, int ovf = ARROW_OVF_NONE) {
+    // caller must be a single lane
+    if (u().status == ARROW_OK) {
+      u().status = s;
+      if (ovf != ARROW_OVF_NONE) u().overflow = ovf;
+    }
+  }
+
+  AS_HD uint32_t next_seq() {
+    uint32_t s = u().seq++;
+    if (s >= SEQ_LIMIT) set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_SEQ);
+    return s;
+  }
+
+  // ------------------------------------------------------ warp argmin --
+
+  AS_HD int warp_argmin(uint64_t key, uint32_t tie, bool valid) {
+    if (w.ballot(valid) == 0) return -1;
+    uint64_t k = valid ? key : ~0ull;
+    uint32_t t = valid ? tie : ~0u;
+    uint32_t hi = w.min_u32((uint32_t)(k >> 32));
+    bool m = valid && (uint32_t)(k >> 32) == hi;
+    uint32_t lo = w.min_u32(m ? (uint32_t)k : ~0u);
+    m = m && (uint32_t)k == lo;
+    uint32_t tt = w.min_u32(m ? t : ~0u);
+    m = m && t == tt;
+    return ffs32(w.ballot(m));
+  }
+
+  // First minimum over instances selected by kf (key, tie); returns the
+  // instance id or -1 (scheduler.py:89-99: strict `<` in insertion order).
+  template <class KF>
+  AS_HD int argmin_inst(KF kf) {
+    uint64_t bk = ~0ull;
+    uint32_t bt = ~0u;
+    int bid = -1;
+#pragma unroll
+    for (int k = 0; k < IPL; k++) {
+      if (st[k].id < 0) continue;
+      uint64_t key;
+      uint32_t tie;
+      if (!kf(st[k], key, tie)) continue;
+      if (bid < 0 || key < bk || (key == bk && tie < bt)) {
+        bk = key;
+        bt = tie;
+        bid = st[k].id;
+      }
+    }
+    int wl = warp_argmin(bk, bt, bid >= 0);
+    if (wl < 0) return -1;
+    return w.shfl(bid, wl);
+  }
+
+  AS_HD int pool_of(int id) const { return sm->pool_of[id]; }
+  AS_HD int pos_of(int id) const { return sm->pos_of[id]; }
+
+  // ---------------------------------------------------- global memory --
+
+  AS_HD int* wp_rid(int id) { return p.wp_rid + (int64_t)id * L.qcap; }
+  AS_HD double* wp_term(int id) { return p.wp_term + (int64_t)id * L.qcap; }
+  AS_HD int* wd_rid(int id) { return p.wd_rid + (int64_t)id * L.qcap; }
+  AS_HD int* mq_rid(int id) { return p.mq_rid + (int64_t)id * L.qcap; }
+  AS_HD int* run_rid(int id) { return p.run_rid + (int64_t)id * L.rcap; }
+  AS_HD int* run_f(int id) { return p.run_f + (int64_t)id * L.rcap; }
+  AS_HD double* em(int id) { return p.em + (int64_t)id * L.ecap; }
+
+  AS_HD int ring(int h, int j, int64_t cap) const {
+    int64_t x = (int64_t)h + j;
+    return (int)(x >= cap ? x - cap : x);
+  }
+
+  // -------------------------------------------- instance-local (owner) --
+
+  AS_HD bool has_prefill_work(const Inst& I) const { return I.rp_rid >= 0 || I.wp_c > 0; }
+  AS_HD bool has_decode_work(const Inst& I) const { return I.mig_active || I.mq_c > 0 || I.R > 0 || I.wd_c > 0; }
+  AS_HD bool startable(const Inst& I) const { return I.R > 0 || I.rp_rid >= 0 || I.wp_c > 0 || I.wd_c > 0; }
+
+  // predicted_prefill_delay, instance.py:304-321 (left fold, same order)
+  AS_HD double delay(const Inst& I, double now) {
+    const arrow_scenario_t& s = sc();
+    double d = 0.0;
+    if (I.busy) {
+      double x = I.busy_until - now;
+      d += (0.0 > x) ? 0.0 : x;
+    }
+    if (I.rp_rid >= 0) d += quad(s.pred_a2, s.pred_a1, s.pred_a0, inl[I.rp_rid] - I.rp_done);
+    const double* t = wp_term(I.id);
+    int h = I.wp_h;
+    int c = I.wp_c;
+    int64_t cap = L.qcap;
+    int j = 0;
+    for (; j + 4 <= c; j += 4) {
+      double t0 = t[ring(h, j, cap)], t1 = t[ring(h, j + 1, cap)];
+      double t2 = t[ring(h, j + 2, cap)], t3 = t[ring(h, j + 3, cap)];
+      d += t0;
+      d += t1;
+      d += t2;
+      d += t3;
+    }
+    for (; j < c; j++) d += t[ring(h, j, cap)];
+    return d;
+  }
+
+  // avg_token_interval, instance.py:323-329.  The ring keeps only emissions
+  // still inside some future query window; cursors only move forward
+  // because simulated time is monotone.
+  AS_HD bool interval(Inst& I, double now, double* out) {
+    double lo = now - sc().window;
+    double* e = em(I.id);
+    while (I.em_c > 0 && e[I.em_h] < lo) {
+      I.em_h = I.em_h + 1 == L.ecap ? 0 : I.em_h + 1;
+      I.em_c--;
+    }
+    if (I.em_c < 2) return false;
+    double first = e[I.em_h];
+    double last = e[ring(I.em_h, I.em_c - 1, L.ecap)];
+    *out = (last - first) / (double)(I.em_c - 1);
+    return true;
+  }
+
+  AS_HD void emit(Inst& I, double now) {
+    double lo = now - sc().window;
+    double* e = em(I.id);
+    while (I.em_c > 0 && e[I.em_h] < lo) {
+      I.em_h = I.em_h + 1 == L.ecap ? 0 : I.em_h + 1;
+      I.em_c--;
+    }
+    if (I.em_c >= L.ecap) {
+      set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_EMISSION);
+      return;
+    }
+    e[ring(I.em_h, I.em_c, L.ecap)] = now;
+    I.em_c++;
+  }
+
+  // advance_migrations, instance.py:126-146 (+ engine push, engine.py:179-181)
+  AS_HD void start_mig(Inst& I, double now) {
+    if (I.mig_active || I.mq_c == 0) return;
+    int rid = mq_rid(I.id)[I.mq_h];
+    int need = inl[rid] + (outl[rid] - 1);
+    int kvf = sc().kv_capacity - I.kv_used - I.kv_reserved - I.committed;
+    if (kvf - I.wgrowth < need) return;
+    I.mq_h = I.mq_h + 1 == L.qcap ? 0 : I.mq_h + 1;
+    I.mq_c--;
+    I.kv_reserved += inl[rid];
+    I.mig_active = 1;
+    I.mig_rid = rid;
+    const arrow_scenario_t& s = sc();
+    I.mig_finish = now + (s.base_latency + (double)((int64_t)inl[rid] * s.bytes_per_token) / s.bandwidth);
+    I.mig_seq = next_seq();
+  }
+
+  // _kick + build_iteration_batch + begin_iteration
+  // (engine.py:170-177, instance.py:175-252)
+  AS_HD void kick(Inst& I, double now) {
+    if (I.busy || !startable(I)) return;
+    const arrow_scenario_t& s = sc();
+    const int budget = s.chunk_budget;
+    const int dcap = imin(s.max_batch, budget);
+    int kvf = s.kv_capacity - I.kv_used - I.kv_reserved - I.committed;
+    if (I.R > dcap) {
+      set_status(ARROW_INTERNAL);
+      return;
+    }
+    int nd = I.R, ad = 0;
+    const int* wd = wd_rid(I.id);
+    while (ad < I.wd_c && nd < dcap) {
+      int rid = wd[ring(I.wd_h, ad, L.qcap)];
+      int g = outl[rid] - 1;
+      if (g > kvf) break;
+      kvf -= g;
+      nd++;
+      ad++;
+    }
+    int rp_chunk = 0, k = 0, last_chunk = 0, last_comp = 0, ded = 0;
+    int total = nd;
+    const int* wp = wp_rid(I.id);
+    bool planned = false;
+    if (nd == 0 && I.rp_rid < 0 && I.wp_c > 0) {
+      int len = inl[wp[I.wp_h]];
+      if (len <= budget && len <= kvf) {
+        k = 1;
+        last_chunk = len;
+        last_comp = 1;
+        ded = 1;
+        total = len;
+        planned = true;
+      }
+    }
+    if (!planned) {
+      int left = budget - nd;
+      bool stop = false;
+      if (I.rp_rid >= 0) {
+        if (left <= 0) {
+          stop = true;
+        } else {
+          int rem = inl[I.rp_rid] - I.rp_done;
+          int c = imin(imin(left, rem), kvf);
+          if (c <= 0) {
+            stop = true;
+          } else {
+            rp_chunk = c;
+            left -= c;
+            kvf -= c;
+            total += c;
+          }
+        }
+      }
+      while (!stop && k < I.wp_c) {
+        if (left <= 0) break;
+        int rem = inl[wp[ring(I.wp_h, k, L.qcap)]];
+        int c = imin(imin(left, rem), kvf);
+        if (c <= 0) break;
+        k++;
+        last_chunk = c;
+        last_comp = c == rem;
+        left -= c;
+        kvf -= c;
+        total += c;
+      }
+    }
+    if (nd == 0 && rp_chunk == 0 && k == 0) return;
+    // begin_iteration
+    const int cur = I.it++;
+    if (ad > 0) {
+      int* rr = run_rid(I.id);
+      int* rf = run_f(I.id);
+      int32_t* dit = (B->req_decode_iter && have_om && om.req_offset >= 0) ? B->req_decode_iter + om.req_offset
+                                                                            : (int32_t*)0;
+      for (int j = 0; j < ad; j++) {
+        int rid = wd[ring(I.wd_h, j, L.qcap)];
+        int g = outl[rid] - 1;
+        int f = cur + g - 1;
+        if (I.R >= L.rcap) {
+          set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_RUNNING);
+          return;
+        }
+        rr[I.R] = rid;
+        rf[I.R] = f;
+        I.R++;
+        if (f < I.min_f) I.min_f = f;
+        I.committed += g;
+        I.wgrowth -= g;
+        if (dit) dit[rid] = cur;
+      }
+      I.wd_h = ring(I.wd_h, ad, L.qcap);
+      I.wd_c -= ad;
+    }
+    I.kv_used += total - nd;
+    if (I.kv_used + I.kv_reserved > s.kv_capacity) set_status(ARROW_INTERNAL);
+    I.pb_ndec = nd;
+    I.pb_rp_chunk = rp_chunk;
+    I.pb_k = k;
+    I.pb_last_chunk = last_chunk;
+    I.pb_last_comp = last_comp;
+    I.pb_ded = ded;
+    double dur = ded ? quad(s.true_a2, s.true_a1, s.true_a0, last_chunk) : s.b1 * (double)total + s.b0;
+    I.busy_until = now + dur;
+    I.busy = 1;
+    I.iter_seq = next_seq();
+  }
+
+  // A prompt finished prefill: first token, park its KV, then either the
+  // single-token completion or a PREFILL_COMPLETE push (engine.py:212-218).
+  AS_HD void prefill_finished(Inst& I, int rid, double now) {
+    p.first[rid] = now;
+    if (outl[rid] == 1) {
+      I.kv_used -= inl[rid];      // release_parked, instance.py:120-122
+      p.last[rid] = now;
+      u().completed++;
+    } else {
+      I.parked++;
+      int c = u().fifo_count;
+      int slot = ring(u().fifo_head, c, L.n_max);
+      p.fifo_rid[slot] = rid;
+      p.fifo_src[slot] = I.id;
+      p.fifo_time[slot] = now;
+      p.fifo_seq[slot] = next_seq();
+      u().fifo_count = c + 1;
+    }
+  }
+
+  // ITERATION_COMPLETE on the owner lane: execute_iteration + the engine
+  // handler (instance.py:254-288, engine.py:205-223).  Returns the drained
+  // pool move to perform (-1 none) as dst pool.
+  AS_HD int iteration_complete(Inst& I, double now) {
+    const int cur = I.it - 1;
+    u().n_iters++;
+    if (B->iterlog && have_om && om.iterlog_offset >= 0) {
+      if (cur < om.iterlog_stride)
+        B->iterlog[om.iterlog_offset + (int64_t)I.id * om.iterlog_stride + cur] = now;
+      else if (u().overflow == ARROW_OVF_NONE)
+        u().overflow = ARROW_OVF_ITERLOG;
+    }
+    const int nd = I.pb_ndec;
+    int nfin = 0, npf = 0;
+    if (nd > 0) {
+      I.kv_used += nd;
+      I.committed -= nd;
+      I.rtok += nd;
+      if (I.min_f == cur) {
+        int* rr = run_rid(I.id);
+        int* rf = run_f(I.id);
+        int m = 0x7fffffff;
+        int j = 0;
+        while (j < I.R) {
+          int f = rf[j];
+          if (f == cur) {
+            int rid = rr[j];
+            int held = inl[rid] + outl[rid] - 1;
+            I.kv_used -= held;
+            I.rtok -= held;
+            p.last[rid] = now;
+            nfin++;
+            I.R--;
+            rr[j] = rr[I.R];
+            rf[j] = rf[I.R];
+          } else {
+            if (f < m) m = f;
+            j++;
+          }
+        }
+        I.min_f = m;
+      }
+    }
+    if (I.pb_rp_chunk > 0) {
+      I.rp_done += I.pb_rp_chunk;
+      if (I.rp_done == inl[I.rp_rid]) {
+        int rid = I.rp_rid;
+        I.rp_rid = -1;
+        npf++;
+        prefill_finished(I, rid, now);
+      }
+    }
+    if (I.pb_k > 0) {
+      const int* wp = wp_rid(I.id);
+      for (int j = 0; j < I.pb_k; j++) {
+        int rid = wp[ring(I.wp_h, j, L.qcap)];
+        if (j < I.pb_k - 1 || I.pb_last_comp) {
+          npf++;
+          prefill_finished(I, rid, now);
+        } else {
+          I.rp_rid = rid;
+          I.rp_done = I.pb_last_chunk;
+        }
+      }
+      I.wp_h = ring(I.wp_h, I.pb_k, L.qcap);
+      I.wp_c -= I.pb_k;
+    }
+    I.busy = 0;
+    I.pb_ndec = I.pb_rp_chunk = I.pb_k = I.pb_last_chunk = I.pb_last_comp = I.pb_ded = 0;
+    if (nd + npf > 0) {
+      emit(I, now);
+      u().esp = 0;
+    }
+    u().completed += nfin;
+    // _check_drained (engine.py:183-192): decided here, applied by the warp
+    int dst = -1;
+    int pk = pool_of(I.id);
+    if (pk == P_P2D && !has_prefill_work(I))
+      dst = P_DECODE;
+    else if (pk == P_D2P && !has_decode_work(I))
+      dst = P_PREFILL;
+    start_mig(I, now);
+    kick(I, now);
+    return dst;
+  }
+
+  // ------------------------------------------------------ decisions ----
+
+  AS_HD void log_decision(double now, int kind, int rid, int inst, int code) {
+    // lane 0 only
+    Uniform& U = u();
+    uint64_t h = U.hash;
+    h = (h ^ dbits(now)) * 1099511628211ull;
+    uint64_t w2 = (uint64_t)kind | ((uint64_t)code << 8) | ((uint64_t)(uint16_t)inst << 16) |
+                  ((uint64_t)(uint32_t)rid << 32);
+    h = (h ^ w2) * 1099511628211ull;
+    U.hash = h;
+    if (B->decisions && have_om && om.decision_offset >= 0) {
+      if (U.n_dec < om.decision_capacity) {
+        arrow_decision_t* d = B->decisions + om.decision_offset + U.n_dec;
+        d->time = now;
+        d->request = rid;
+        d->instance = (int16_t)inst;
+        d->kind = (uint8_t)kind;
+        d->code = (uint8_t)code;
+      } else if (U.overflow == ARROW_OVF_NONE) {
+        U.overflow = ARROW_OVF_DECISIONS;
+      }
+    }
+    U.n_dec++;
+  }
+
+  AS_HD void log_dispatch(double now, int kind, int rid, int inst, int branch) {
+    lane0([&] {
+      log_decision(now, kind, rid, inst, branch);
+      if (have_om && om.req_offset >= 0) {
+        int32_t* out = kind == ARROW_DEC_PREFILL_DISPATCH ? B->req_prefill : B->req_decode;
+        if (out) out[om.req_offset + rid] = inst | (branch << 16);
+      }
+    });
+  }
+
+  // PoolSet._move (pools.py:76-85) + the flip record (scheduler.py:109-119).
+  AS_HD void move_and_log(int id, int dst, double now, int trigger) {
+    int src = pool_of(id);
+    int pos = pos_of(id);
+    w.sync();
+    for (int y = lane; y < MAX_INST; y += WD)
+      if (y < sc().n_instances && y != id && sm->pool_of[y] == src && sm->pos_of[y] > pos) sm->pos_of[y]--;
+    w.sync();
+    lane0([&] {
+      Uniform& U = u();
+      sm->pool_of[id] = (int16_t)dst;
+      sm->pos_of[id] = (int16_t)U.pool_n[dst];
+      U.pool_n[src]--;
+      U.pool_n[dst]++;
+      U.n_flips++;
+      log_decision(now, ARROW_DEC_FLIP, -1, id, trigger | (src << 3) | (dst << 5));
+    });
+  }
+
+  // ---------------------------------------------------- scheduler ------
+
+  AS_HD void compute_delays(double now) {
+#pragma unroll
+    for (int k = 0; k < IPL; k++)
+      if (st[k].id >= 0) st[k].dly = delay(st[k], now);
+  }
+
+  // _argmin over one pool (insertion order), key = delay
+  AS_HD int argmin_delay_pool(int pool) {
+    return argmin_inst([&](Inst& I, uint64_t& key, uint32_t& tie) {
+      if (pool_of(I.id) != pool) return false;
+      key = okey(I.dly);
+      tie = (uint32_t)pos_of(I.id);
+      return true;
+    });
+  }
+
+  AS_HD int argmin_tokens_pool(int pool) {
+    return argmin_inst([&](Inst& I, uint64_t& key, uint32_t& tie) {
+      if (pool_of(I.id) != pool) return false;
+      key = (uint64_t)(uint32_t)I.rtok;
+      tie = (uint32_t)pos_of(I.id);
+      return true;
+    });
+  }
+
+  // members(DECODE) + members(P_TO_D) order
+  AS_HD uint32_t decode_role_tie(int id) const {
+    return (pool_of(id) == P_DECODE ? 0u : 256u) + (uint32_t)pos_of(id);
+  }
+
+  AS_HD bool decode_role(int id) const { return pool_of(id) == P_DECODE || pool_of(id) == P_P2D; }
+
+  // _pool_mean_interval (scheduler.py:124-134): ordered Neumaier sum of the
+  // non-None intervals of DECODE then P_TO_D members, divided by the count.
+  AS_HD bool pool_mean_interval(double now, double* out) {
+    const int nD = u().pool_n[P_DECODE];
+    const int m = nD + u().pool_n[P_P2D];
+#pragma unroll
+    for (int k = 0; k < IPL; k++) {
+      Inst& I = st[k];
+      if (I.id < 0 || !decode_role(I.id)) continue;
+      int cpos = pool_of(I.id) == P_DECODE ? pos_of(I.id) : nD + pos_of(I.id);
+      double v = 0.0;
+      bool ok = interval(I, now, &v);
+      sm->vals[cpos] = v;
+      sm->valid[cpos] = ok ? 1 : 0;
+    }
+    w.sync();
+    double f = 0.0, c = 0.0;
+    int cnt = 0;
+    for (int j = 0; j < m; j++) {
+      if (!sm->valid[j]) continue;
+      double x = sm->vals[j];
+      if (cnt == 0) {
+        f = 0.0 + x;
+      } else {
+        double t = f + x;
+        if (fabs(f) >= fabs(x))
+          c += (f - t) + x;
+        else
+          c += (x - t) + f;
+        f = t;
+      }
+      cnt++;
+    }
+    w.sync();
+    if (cnt == 0) return false;
+    if (c != 0.0 && isfinite(c)) f += c;
+    *out = f / (double)cnt;
+    return true;
+  }
+
+  // decode_load_is_low, scheduler.py:136-147
+  AS_HD bool decode_load_is_low(double now) {
+    bool mine = false;
+    uint32_t mn = ~0u;
+#pragma unroll
+    for (int k = 0; k < IPL; k++) {
+      if (st[k].id >= 0 && decode_role(st[k].id)) {
+        mine = true;
+        if ((uint32_t)st[k].rtok < mn) mn = (uint32_t)st[k].rtok;
+      }
+    }
+    if (w.ballot(mine) == 0) return false;
+    uint32_t min_tokens = w.min_u32(mn);
+    if ((double)min_tokens > sc().theta_d * (double)sc().max_tokens) return false;
+    double mean;
+    if (!pool_mean_interval(now, &mean)) return true;
+    return mean <= sc().tpot_thr;
+  }
+
+  // try_move_decode_to_prefill, scheduler.py:258-276
+  AS_HD int try_move_d2p(double now, int trigger) {
+    if (!sc().enable_flips) return -1;
+    if (u().pool_n[P_DECODE] + u().pool_n[P_P2D] <= 1) return -1;
+    int cand = u().pool_n[P_P2D] > 0 ? P_P2D : P_DECODE;
+    int chosen = argmin_tokens_pool(cand);
+    int hdw = bcast_i(chosen, [&](Inst& I) { return has_decode_work(I) ? 1 : 0; });
+    int dst = cand == P_DECODE ? (hdw ? P_D2P : P_PREFILL) : P_PREFILL;
+    move_and_log(chosen, dst, now, trigger);
+    return chosen;
+  }
+
+  // try_move_prefill_to_decode, scheduler.py:278-296 (delays must be current)
+  AS_HD int try_move_p2d(double now, int trigger) {
+    if (!sc().enable_flips) return -1;
+    if (u().pool_n[P_PREFILL] + u().pool_n[P_D2P] <= 1) return -1;
+    int cand = u().pool_n[P_D2P] > 0 ? P_D2P : P_PREFILL;
+    int chosen = argmin_delay_pool(cand);
+    int hpw = bcast_i(chosen, [&](Inst& I) { return has_prefill_work(I) ? 1 : 0; });
+    int dst = cand == P_PREFILL ? (hpw ? P_P2D : P_DECODE) : P_DECODE;
+    move_and_log(chosen, dst, now, trigger);
+    return chosen;
+  }
+
+  AS_HD int rr_pick(int pool, int64_t counter) {
+    int n = u().pool_n[pool];
+    int want = (int)(counter % n);
+    int id = -1;
+#pragma unroll
+    for (int k = 0; k < IPL; k++)
+      if (st[k].id >= 0 && pool_of(st[k].id) == pool && pos_of(st[k].id) == want) id = st[k].id;
+    uint32_t b = w.ballot(id >= 0);
+    return w.shfl(id, ffs32(b));
+  }
+
+  // schedule_prefill, scheduler.py:151-195
+  AS_HD int schedule_prefill(int rid, double now, double own) {
+    const int K = ARROW_DEC_PREFILL_DISPATCH;
+    const int strat = sc().strategy;
+    if (strat == ARROW_STRATEGY_ROUND_ROBIN) {
+      int chosen = rr_pick(P_PREFILL, u().rr_p);
+      w.sync();
+      lane0([&] { u().rr_p++; });
+      log_dispatch(now, K, rid, chosen, ARROW_BR_ROUND_ROBIN);
+      return chosen;
+    }
+    compute_delays(now);
+    if (strat == ARROW_STRATEGY_MINIMAL_LOAD) {
+      int chosen = argmin_delay_pool(P_PREFILL);
+      log_dispatch(now, K, rid, chosen, ARROW_BR_MIN_LOAD);
+      return chosen;
+    }
+    const double thr = sc().ttft_thr;
+    int t1 = argmin_delay_pool(P_PREFILL);
+    if (t1 >= 0) {
+      double d1 = bcast_d(t1, [](Inst& I) { return I.dly; });
+      if (d1 + own <= thr) {
+        log_dispatch(now, K, rid, t1, ARROW_BR_ALG1_T1);
+        return t1;
+      }
+    }
+    int t2 = argmin_delay_pool(P_D2P);
+    if (t2 >= 0) {
+      double d2 = bcast_d(t2, [](Inst& I) { return I.dly; });
+      if (d2 + own <= thr) {
+        log_dispatch(now, K, rid, t2, ARROW_BR_ALG1_T2);
+        return t2;
+      }
+    }
+    if (sc().enable_flips && decode_load_is_low(now)) {
+      int t3 = try_move_d2p(now, ARROW_TRIG_ALG1);
+      if (t3 >= 0) {
+        log_dispatch(now, K, rid, t3, ARROW_BR_ALG1_FLIP);
+        return t3;
+      }
+    }
+    if (t1 >= 0) {
+      log_dispatch(now, K, rid, t1, ARROW_BR_ALG1_FALLBACK);
+      return t1;
+    }
+    if (t2 >= 0) {
+      log_dispatch(now, K, rid, t2, ARROW_BR_ALG1_FALLBACK);
+      return t2;
+    }
+    int chosen = argmin_inst([&](Inst& I, uint64_t& key, uint32_t& tie) {
+      if (!decode_role(I.id)) return false;
+      key = okey(I.dly);
+      tie = decode_role_tie(I.id);
+      return true;
+    });
+    if (chosen < 0) {
+      lane0([&] { set_status(ARROW_NO_INSTANCE); });
+      return -1;
+    }
+    log_dispatch(now, K, rid, chosen, ARROW_BR_ALG1_DEGENERATE);
+    return chosen;
+  }
+
+  // _decode_admissible, scheduler.py:214-218
+  AS_HD bool decode_admissible(int id, int tokens, double now) {
+    if ((int64_t)tokens > sc().max_tokens) return false;
+    int r = 0;
+    owner(id, [&](Inst& I) {
+      double v;
+      r = interval(I, now, &v) ? (v <= sc().tpot_thr ? 1 : 0) : 1;
+      u().tmp_i[0] = r;
+    });
+    const bool ok = u().tmp_i[0] != 0;
+    w.sync();
+    return ok;
+  }
+
+  // schedule_decode, scheduler.py:199-254
+  AS_HD int schedule_decode(int rid, int src, double now) {
+    const int K = ARROW_DEC_DECODE_DISPATCH;
+    const int strat = sc().strategy;
+    if (strat == ARROW_STRATEGY_ROUND_ROBIN) {
+      int chosen = rr_pick(P_DECODE, u().rr_d);
+      w.sync();
+      lane0([&] { u().rr_d++; });
+      log_dispatch(now, K, rid, chosen, ARROW_BR_ROUND_ROBIN);
+      return chosen;
+    }
+    if (strat == ARROW_STRATEGY_MINIMAL_LOAD) {
+      int chosen = argmin_tokens_pool(P_DECODE);
+      log_dispatch(now, K, rid, chosen, ARROW_BR_MIN_LOAD);
+      return chosen;
+    }
+    if (decode_role(src)) {
+      log_dispatch(now, K, rid, src, ARROW_BR_ALG2_ZERO_TRANSFER);
+      return src;
+    }
+    int t1 = argmin_tokens_pool(P_DECODE);
+    int tok1 = t1 >= 0 ? bcast_i(t1, [](Inst& I) { return I.rtok; }) : 0;
+    if (t1 >= 0 && decode_admissible(t1, tok1, now)) {
+      log_dispatch(now, K, rid, t1, ARROW_BR_ALG2_T1);
+      return t1;
+    }
+    int t2 = argmin_tokens_pool(P_P2D);
+    int tok2 = t2 >= 0 ? bcast_i(t2, [](Inst& I) { return I.rtok; }) : 0;
+    if (t2 >= 0 && decode_admissible(t2, tok2, now)) {
+      log_dispatch(now, K, rid, t2, ARROW_BR_ALG2_T2);
+      return t2;
+    }
+    if (sc().enable_flips) {
+      compute_delays(now);
+      int t3 = try_move_p2d(now, ARROW_TRIG_ALG2);
+      if (t3 >= 0) {
+        log_dispatch(now, K, rid, t3, ARROW_BR_ALG2_FLIP);
+        return t3;
+      }
+    }
+    if (t1 >= 0 && (t2 < 0 || tok1 <= tok2)) {
+      log_dispatch(now, K, rid, t1, ARROW_BR_ALG2_FALLBACK);
+      return t1;
+    }
+    if (t2 >= 0) {
+      log_dispatch(now, K, rid, t2, ARROW_BR_ALG2_FALLBACK);
+      return t2;
+    }
+    log_dispatch(now, K, rid, src, ARROW_BR_ALG2_FORCED_LOCAL);
+    return src;
+  }
+
+  // ------------------------------------------------------- handlers ----
+
+  AS_HD void on_arrival(double now) {
+    const int rid = u().a;
+    const double own = quad(sc().pred_a2, sc().pred_a1, sc().pred_a0, inl[rid]);
+    w.sync();
+    lane0([&] {
+      Uniform& U = u();
+      U.a = rid + 1;
+      U.next_arrival = U.a < sc().n_requests ? arr[U.a] * sc().arrival_scale : 0.0;
+    });
+    int target = schedule_prefill(rid, now, own);
+    if (target < 0) return;
+    owner(target, [&](Inst& I) {
+      if (I.wp_c >= L.qcap) {
+        set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_QUEUE);
+        return;
+      }
+      int slot = ring(I.wp_h, I.wp_c, L.qcap);
+      wp_rid(I.id)[slot] = rid;
+      wp_term(I.id)[slot] = own;
+      I.wp_c++;
+      kick(I, now);
+    });
+  }
+
+  AS_HD void on_prefill_complete(double now) {
+    int rid = 0, src = 0;
+    {
+      Uniform& U = u();
+      rid = p.fifo_rid[U.fifo_head];
+      src = p.fifo_src[U.fifo_head];
+    }
+    w.sync();
+    lane0([&] {
+      Uniform& U = u();
+      U.fifo_head = U.fifo_head + 1 == L.n_max ? 0 : U.fifo_head + 1;
+      U.fifo_count--;
+    });
+    int target = schedule_decode(rid, src, now);
+    const int in = inl[rid], g = outl[rid] - 1;
+    owner(target, [&](Inst& I) {
+      if (target == src) {
+        I.parked--;           // adopt_local_decode: parked KV becomes the decode's
+      } else {
+        p.src[rid] = src;
+        if (I.mq_c >= L.qcap) {
+          set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_QUEUE);
+          return;
+        }
+        mq_rid(I.id)[ring(I.mq_h, I.mq_c, L.qcap)] = rid;
+        I.mq_c++;
+        start_mig(I, now);
+        kick(I, now);
+        return;
+      }
+      if (I.wd_c >= L.qcap) {
+        set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_QUEUE);
+        return;
+      }
+      wd_rid(I.id)[ring(I.wd_h, I.wd_c, L.qcap)] = rid;
+      I.wd_c++;
+      I.wgrowth += g;
+      I.rtok += in;
+      kick(I, now);
+    });
+  }
+
+  AS_HD void on_migration_complete(int id, double now) {
+    owner(id, [&](Inst& I) {
+      int rid = I.mig_rid;
+      I.mig_active = 0;
+      I.kv_reserved -= inl[rid];
+      I.kv_used += inl[rid];
+      if (I.wd_c >= L.qcap) {
+        set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_QUEUE);
+        return;
+      }
+      wd_rid(I.id)[ring(I.wd_h, I.wd_c, L.qcap)] = rid;
+      I.wd_c++;
+      I.wgrowth += outl[rid] - 1;
+      I.rtok += inl[rid];
+      u().tmp_i[1] = rid;
+      u().tmp_i[2] = p.src[rid];
+    });
+    const int rid = u().tmp_i[1];
+    const int src = u().tmp_i[2];
+    w.sync();
+    owner(src, [&](Inst& S) {
+      S.kv_used -= inl[rid];   // release_parked
+      S.parked--;
+    });
+    owner(id, [&](Inst& I) { start_mig(I, now); });
+    owner(src, [&](Inst& S) { start_mig(S, now); });
+    owner(id, [&](Inst& I) { kick(I, now); });
+    owner(src, [&](Inst& S) { kick(S, now); });
+  }
+
+  AS_HD void write_snapshots(double now) {
+    if (!(B->snapshots && have_om && om.snapshot_offset >= 0)) return;
+    const int N = sc().n_instances;
+    const int64_t base = u().n_snap;
+#pragma unroll
+    for (int k = 0; k < IPL; k++) {
+      Inst& I = st[k];
+      if (I.id < 0) continue;
+      int64_t slot = base + I.id;
+      if (slot >= om.snapshot_capacity) continue;
+      arrow_snapshot_t* s = B->snapshots + om.snapshot_offset + slot;
+      double iv = 0.0;
+      bool ok = interval(I, now, &iv);
+      s->time = now;
+      s->pred_delay = delay(I, now);
+      s->avg_interval = ok ? iv : NAN;
+      s->instance = I.id;
+      s->pool = pool_of(I.id);
+      s->running_tokens = I.rtok;
+      s->kv_used = I.kv_used;
+      s->queue_len = I.wp_c - I.pb_k;
+      s->prefill_count = (I.rp_rid >= 0 ? 1 : 0) + I.wp_c;
+      s->decode_count = I.R + I.wd_c + I.mq_c + (I.mig_active ? 1 : 0);
+      s->reserved = 0;
+    }
+    w.sync();
+    lane0([&] {
+      if (base + N > om.snapshot_capacity && u().overflow == ARROW_OVF_NONE) u().overflow = ARROW_OVF_SNAPSHOTS;
+      u().n_snap = base + N;
+    });
+  }
+
+  // scheduler.monitor_tick, scheduler.py:300-335.  Returns true when the
+  // tick changed nothing and the decode pool reported no interval (the
+  // fixed point the stall fast path relies on).
+  AS_HD bool monitor_tick(double now) {
+    const arrow_scenario_t& s = sc();
+    if (s.strategy != ARROW_STRATEGY_SLO_AWARE || !s.enable_flips) return true;
+    const int flips0 = u().n_flips;
+    double mean = 0.0;
+    bool have = pool_mean_interval(now, &mean);
+    if (have && mean > s.tpot_thr) {
+      lane0([&] { u().breach += s.monitor_period; });
+      if (u().breach >= s.breach_duration) {
+        compute_delays(now);
+        try_move_p2d(now, ARROW_TRIG_MONITOR_TPOT);
+      }
+    } else {
+      lane0([&] { u().breach = 0.0; });
+    }
+    // aggregate decode load over DECODE + P_TO_D
+    uint64_t agg = 0;
+    bool mine = false;
+#pragma unroll
+    for (int k = 0; k < IPL; k++)
+      if (st[k].id >= 0 && decode_role(st[k].id)) {
+        agg += (uint64_t)(uint32_t)st[k].rtok;
+        mine = true;
+      }
+    uint32_t members = w.ballot(mine);
+    if (members == 0) return !have && u().n_flips == flips0;
+    for (int off = WD / 2; off > 0; off >>= 1) agg += w.shfl(agg, (lane + off) & (WD - 1));
+    agg = w.shfl(agg, 0);
+    int m = 0;
+    {
+      int c = 0;
+#pragma unroll
+      for (int k = 0; k < IPL; k++) c += (st[k].id >= 0 && decode_role(st[k].id)) ? 1 : 0;
+      m = (int)w.add_u32((uint32_t)c);
+    }
+    int64_t capacity = s.max_tokens * (int64_t)m;
+    if (capacity == 0) {
+      lane0([&] { set_status(ARROW_ZERO_DIVISION); });
+      return false;
+    }
+    if ((double)agg / (double)capacity <= s.theta_busy) return !have && u().n_flips == flips0;
+    // snapshot of PREFILL members in insertion order
+    const int np = u().pool_n[P_PREFILL];
+#pragma unroll
+    for (int k = 0; k < IPL; k++)
+      if (st[k].id >= 0 && pool_of(st[k].id) == P_PREFILL) sm->list[pos_of(st[k].id)] = st[k].id;
+    w.sync();
+    for (int j = 0; j < np; j++) {
+      if (u().pool_n[P_PREFILL] + u().pool_n[P_D2P] <= 1) break;
+      int x = sm->list[j];
+      int busy_or_work = bcast_i(x, [&](Inst& I) { return (has_prefill_work(I) || I.busy) ? 1 : 0; });
+      if (busy_or_work) continue;
+      move_and_log(x, P_DECODE, now, ARROW_TRIG_MONITOR_IDLE);
+    }
+    w.sync();
+    return !have && u().n_flips == flips0;
+  }
+
+  // ----------------------------------------------------- event loop ----
+
+  AS_HD void init_scenario(int s) {
+    sid = s;
+    have_om = B->outmap != 0;
+    if (have_om) om = B->outmap[s];
+    lane0([&] {
+      sm->sc = B->scenarios[s];
+      Uniform& U = u();
+      memset(&U, 0, sizeof(U));
+      U.status = ARROW_OK;
+      U.hash = 14695981039346656037ull;
+      U.stall_time = NAN;
+      const arrow_scenario_t& c = sm->sc;
+      for (int i = 0; i < c.n_instances; i++) {
+        int k = i < c.n_prefill_init ? P_PREFILL : P_DECODE;
+        sm->pool_of[i] = (int16_t)k;
+        sm->pos_of[i] = (int16_t)U.pool_n[k];
+        U.pool_n[k]++;
+      }
+      U.seq = (uint32_t)c.n_requests;
+      if (c.n_requests > 0) {
+        U.tick_active = 1;
+        U.tick_time = c.monitor_period;
+        U.tick_seq = U.seq++;
+      }
+      U.a = 0;
+      U.next_arrival = c.n_requests > 0 ? B->arrival[c.trace_offset] * c.arrival_scale : 0.0;
+    });
+    const arrow_scenario_t& c = sc();
+    arr = B->arrival + c.trace_offset;
+    inl = B->input_len + c.trace_offset;
+    outl = B->output_len + c.trace_offset;
+#pragma unroll
+    for (int k = 0; k < IPL; k++) {
+      Inst& I = st[k];
+      memset(&I, 0, sizeof(I));
+      int id = lane + k * WD;
+      I.id = id < c.n_instances ? id : -1;
+      I.rp_rid = -1;
+      I.min_f = 0x7fffffff;
+      I.mig_rid = -1;
+    }
+    int32_t* rpf = (have_om && om.req_offset >= 0) ? B->req_prefill : 0;
+    int32_t* rdc = (have_om && om.req_offset >= 0) ? B->req_decode : 0;
+    int32_t* rdi = (have_om && om.req_offset >= 0) ? B->req_decode_iter : 0;
+    for (int r = lane; r < c.n_requests; r += WD) {
+      p.first[r] = NAN;
+      p.last[r] = NAN;
+      if (rpf) rpf[om.req_offset + r] = -1;
+      if (rdc) rdc[om.req_offset + r] = -1;
+      if (rdi) rdi[om.req_offset + r] = -1;
+    }
+    w.sync();
+  }
+
+  // Next event: lexicographic (time, kind, seq) minimum over every pending
+  // event (engine.py:267).  Returns the event code: 2*inst + kind for
+  // instance events, 1000 + kind for global ones, -1 when the heap is empty.
+  AS_HD int next_event(double* when) {
+    uint64_t bk = ~0ull;
+    uint32_t bs = ~0u;
+    int code = -1;
+    auto offer = [&](double t, int kind, uint32_t seq, int c) {
+      uint64_t k1 = okey(t);
+      uint32_t k2 = ((uint32_t)kind << 28) | seq;
+      if (code < 0 || k1 < bk || (k1 == bk && k2 < bs)) {
+        bk = k1;
+        bs = k2;
+        code = c;
+      }
+    };
+#pragma unroll
+    for (int k = 0; k < IPL; k++) {
+      const Inst& I = st[k];
+      if (I.id < 0) continue;
+      if (I.busy) offer(I.busy_until, EV_ITER, I.iter_seq, 2 * I.id + 1);
+      if (I.mig_active) offer(I.mig_finish, EV_MIG, I.mig_seq, 2 * I.id);
+    }
+    if (lane == 0) {
+      const Uniform& U = sm->u;
+      if (U.a < sc().n_requests) offer(U.next_arrival, EV_ARRIVAL, (uint32_t)U.a, 1000 + EV_ARRIVAL);
+      if (U.fifo_count > 0) offer(p.fifo_time[U.fifo_head], EV_PREFILL, p.fifo_seq[U.fifo_head], 1000 + EV_PREFILL);
+      if (U.tick_active) offer(U.tick_time, EV_TICK, U.tick_seq, 1000 + EV_TICK);
+    }
+    int wl = warp_argmin(bk, bs, code >= 0);
+    if (wl < 0) return -1;
+    *when = okey_inv(w.shfl(bk, wl));
+    return w.shfl(code, wl);
+  }
+
+  AS_HD bool only_tick_pending() {
+    bool active = false;
+#pragma unroll
+    for (int k = 0; k < IPL; k++) active = active || (st[k].id >= 0 && (st[k].busy || st[k].mig_active));
+    if (w.any(active)) return false;
+    const Uniform& U = sm->u;
+    return U.a >= sc().n_requests && U.fifo_count == 0 && U.tick_active && U.completed < sc().n_requests;
+  }
+
+  AS_HD void simulate() {
+    const int64_t limit = sc().stall_limit;
+    for (;;) {
+      w.sync();
+      double now = 0.0;
+      int ev = next_event(&now);
+      if (ev < 0) break;
+      lane0([&] {
+        u().now = now;
+        u().esp++;
+        u().n_events++;
+        ATRACE("ev %d t=%.17g esp=%lld\n", ev, now, (long long)u().esp);
+      });
+      if (ev >= 1000) {
+        int kind = ev - 1000;
+        if (kind == EV_ARRIVAL) {
+          on_arrival(now);
+        } else if (kind == EV_PREFILL) {
+          on_prefill_complete(now);
+        } else {
+          lane0([&] { u().n_ticks++; });
+          write_snapshots(now);
+          bool fixed = monitor_tick(now);
+          bool idle = only_tick_pending();
+          bool healthy = u().status == ARROW_OK && u().esp <= limit;
+          w.sync();
+          lane0([&] {
+            Uniform& U = u();
+            if (U.completed < sc().n_requests) {
+              U.tick_time = now + sc().monitor_period;
+              U.tick_seq = next_seq();
+            } else {
+              U.tick_active = 0;
+            }
+          });
+          if (fixed && idle && healthy) {
+            // Nothing but ticks can ever happen again and each tick is a
+            // no-op: count them down to the watchdog (engine.py:283-284).
+            lane0([&] {
+              Uniform& U = u();
+              double t = now;
+              while (U.esp <= limit) {
+                t = U.tick_time;
+                U.tick_time = t + sc().monitor_period;
+                U.esp++;
+                U.n_events++;
+                U.n_ticks++;
+              }
+              U.now = t;
+            });
+            now = u().now;
+          }
+        }
+      } else {
+        int id = ev >> 1;
+        if (ev & 1) {
+          int dst = -1;
+          owner(id, [&](Inst& I) { u().tmp_i[0] = iteration_complete(I, now); });
+          dst = u().tmp_i[0];
+          w.sync();
+          if (dst >= 0) move_and_log(id, dst, now, ARROW_TRIG_DRAINED);
+        } else {
+          on_migration_complete(id, now);
+        }
+      }
+      const int status = u().status;
+      const int64_t esp = u().esp;
+      w.sync();
+      if (status != ARROW_OK) return;
+      if (esp > limit) {
+        lane0([&] {
+          u().status = ARROW_STALLED;
+          u().stall_time = now;
+        });
+        return;
+      }
+    }
+    // end-of-run checks, engine.py:286-290
+    const int completed = u().completed;
+    w.sync();
+    if (completed != sc().n_requests) {
+      lane0([&] { u().status = ARROW_INCOMPLETE; });
+      return;
+    }
+    bool dirty = false;
+#pragma unroll
+    for (int k = 0; k < IPL; k++) {
+      const Inst& I = st[k];
+      if (I.id < 0) continue;
+      dirty = dirty || I.busy || I.R || I.rp_rid >= 0 || I.wp_c || I.wd_c || I.mq_c || I.mig_active ||
+              I.parked || I.kv_used || I.kv_reserved;
+    }
+    if (w.any(dirty)) lane0([&] { u().status = ARROW_NOT_DRAINED; });
+  }
+
+  AS_HD void write_diag() {
+    if (!(B->diag && have_om && om.diag_offset >= 0)) return;
+#pragma unroll
+    for (int k = 0; k < IPL; k++) {
+      const Inst& I = st[k];
+      if (I.id < 0) continue;
+      arrow_instdiag_t* d = B->diag + om.diag_offset + I.id;
+      d->busy_until = I.busy ? I.busy_until : NAN;
+      d->pool = pool_of(I.id);
+      d->kv_used = I.kv_used;
+      d->running = I.R + (I.rp_rid >= 0 ? 1 : 0) + (I.busy ? I.pb_k : 0);
+      d->waiting = (I.wp_c - (I.busy ? I.pb_k : 0)) + I.wd_c;
+      d->migrating = I.mq_c;
+      d->reserved = 0;
+    }
+    w.sync();
+  }
+
+  // Radix select of the k-th smallest (0-based) non-negative double.
+  AS_HD double select_kth(const double* v, int n, int kth) {
+    uint64_t prefix = 0, mask = 0;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int b = lane; b < 256; b += WD) sm->hist[b] = 0;
+      w.sync();
+      for (int i = lane; i < n; i += WD) {
+        uint64_t key = okey(v[i]);
+        if ((key & mask) == prefix) w.atomic_add_shared(&sm->hist[(key >> shift) & 255], 1);
+      }
+      w.sync();
+      lane0([&] {
+        int acc = 0, b = 0;
+        for (; b < 256; b++) {
+          if (acc + sm->hist[b] > u().tmp_i[3]) break;
+          acc += sm->hist[b];
+        }
+        u().tmp_i[3] -= acc;
+        u().tmp_i[2] = b;
+      });
+      prefix |= (uint64_t)u().tmp_i[2] << shift;
+      mask |= (uint64_t)255 << shift;
+      w.sync();
+    }
+    return okey_inv(prefix);
+  }
+
+  // compute_metrics over the run's records (report.py:55-74, core.py:105-156)
+  AS_HD void summarize(arrow_summary_t* out) {
+    const arrow_scenario_t& c = sc();
+    const int n = c.n_requests;
+    uint32_t ok_cnt = 0;
+    uint64_t kmax = 0, kmin = ~0ull;
+    for (int r = lane; r < n; r += WD) {
+      double a = arr[r] * c.arrival_scale;
+      double f = p.first[r], l = p.last[r];
+      int m = outl[r];
+      double tt = f - a;
+      double tp = m == 1 ? 0.0 : (l - f) / (double)(m - 1);
+      p.ttft[r] = tt;
+      p.tpot[r] = tp;
+      ok_cnt += (tt <= c.ttft_slo && tp <= c.tpot_slo) ? 1u : 0u;
+      uint64_t kl = okey(l), ka = okey(a);
+      if (kl > kmax) kmax = kl;
+      if (ka < kmin) kmin = ka;
+    }
+    uint32_t n_ok = w.add_u32(ok_cnt);
+    // 64-bit max/min via two-step 32-bit redux
+    uint32_t hi = w.max_u32((uint32_t)(kmax >> 32));
+    uint32_t lo = w.max_u32((uint32_t)(kmax >> 32) == hi ? (uint32_t)kmax : 0u);
+    double maxlast = okey_inv(((uint64_t)hi << 32) | lo);
+    hi = w.min_u32((uint32_t)(kmin >> 32));
+    lo = w.min_u32((uint32_t)(kmin >> 32) == hi ? (uint32_t)kmin : ~0u);
+    double minarr = okey_inv(((uint64_t)hi << 32) | lo);
+    w.sync();
+    int rank = (int)ceil(0.9 * (double)n);
+    if (rank < 1) rank = 1;
+    lane0([&] { u().tmp_i[3] = rank - 1; });
+    double p90_ttft = select_kth(p.ttft, n, rank - 1);
+    lane0([&] { u().tmp_i[3] = rank - 1; });
+    double p90_tpot = select_kth(p.tpot, n, rank - 1);
+    if (lane == 0) {
+      // Python sum(): CPython 3.12 Neumaier loop, request order
+      double sums[2];
+      for (int which = 0; which < 2; which++) {
+        const double* v = which == 0 ? p.ttft : p.tpot;
+        double f = 0.0 + v[0], cc = 0.0;
+        for (int i = 1; i < n; i++) {
+          double x = v[i];
+          double t = f + x;
+          if (fabs(f) >= fabs(x))
+            cc += (f - t) + x;
+          else
+            cc += (x - t) + f;
+          f = t;
+        }
+        if (cc != 0.0 && isfinite(cc)) f += cc;
+        sums[which] = f;
+      }
+      out->n_ok = (int32_t)n_ok;
+      out->attainment = (double)n_ok / (double)n;
+      out->mean_ttft = sums[0] / (double)n;
+      out->mean_tpot = sums[1] / (double)n;
+      out->p90_ttft = p90_ttft;
+      out->p90_tpot = p90_tpot;
+      out->span = maxlast - minarr;
+      out->goodput = out->span > 0 ? (double)n_ok / out->span : INFINITY;
+    }
+    w.sync();
+  }
+
+  AS_HD void finish() {
+    arrow_summary_t* out = B->summaries + sid;
+    const Uniform& U = sm->u;
+    if (U.status == ARROW_STALLED || U.status == ARROW_INCOMPLETE) write_diag();
+    if (lane == 0) {
+      memset(out, 0, sizeof(*out));
+      out->status = U.status;
+      out->overflow = U.overflow;
+      out->n_requests = sc().n_requests;
+      out->n_completed = U.completed;
+      out->n_flips = U.n_flips;
+      out->n_events = U.n_events;
+      out->n_iterations = U.n_iters;
+      out->n_decisions = U.n_dec;
+      out->n_ticks = U.n_ticks;
+      out->n_snapshots = U.n_snap;
+      out->stall_time = U.status == ARROW_STALLED ? U.stall_time : NAN;
+      out->decision_hash = U.hash;
+      out->attainment = out->p90_ttft = out->p90_tpot = NAN;
+      out->mean_ttft = out->mean_tpot = out->goodput = out->span = NAN;
+    }
+    w.sync();
+    if (U.status == ARROW_OK && sc().n_requests > 0) summarize(out);
+    if (lane == 0 && U.status == ARROW_OK && U.overflow != ARROW_OVF_NONE) out->status = ARROW_BUFFER_OVERFLOW;
+    // per-request outputs
+    if (have_om && om.req_offset >= 0) {
+      for (int r = lane; r < sc().n_requests; r += WD) {
+        if (B->req_first) B->req_first[om.req_offset + r] = p.first[r];
+        if (B->req_last) B->req_last[om.req_offset + r] = p.last[r];
+      }
+    }
+    w.sync();
+  }
+
+  AS_HD void run(int s) {
+    init_scenario(s);
+    simulate();
+    finish();
+  }
+};
+
+}  // namespace arrow

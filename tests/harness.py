@@ -1,0 +1,186 @@
+"""Shared test plumbing: golden fixtures, the CPU oracle, the host SIMT
+emulator of the kernel, and field-by-field comparison helpers.
+
+The oracle (oracle/build/libpdsim_oracle.so) and the emulator
+(build/libarrow_emu.so) are test infrastructure only; the product package
+never loads them.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import json
+import math
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+from paper_2505_11916_b200 import _abi  # noqa: E402
+from paper_2505_11916_b200._buffers import HostBuffers, OutputSpec  # noqa: E402
+from paper_2505_11916_b200._compile import Scenario, TraceEntry, compile_batch  # noqa: E402
+from paper_2505_11916_b200.config import config_from_values  # noqa: E402
+
+GOLDEN = ROOT / "tests" / "golden"
+
+_libs: dict = {}
+
+
+def _build(target: str) -> None:
+    subprocess.run(["make", "-s", "-C", str(ROOT), target], check=True)
+
+
+def oracle_lib() -> ctypes.CDLL:
+    if "oracle" not in _libs:
+        path = ROOT / "oracle" / "build" / "libpdsim_oracle.so"
+        if not path.exists():
+            _build("oracle")
+        lib = ctypes.CDLL(str(path))
+        lib.pdsim_oracle_run_batch.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        lib.pdsim_oracle_run_batch.restype = ctypes.c_int
+        lib.pdsim_oracle_pysum.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+        lib.pdsim_oracle_pysum.restype = ctypes.c_double
+        lib.pdsim_oracle_decision_hash.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+        lib.pdsim_oracle_decision_hash.restype = ctypes.c_uint64
+        _libs["oracle"] = lib
+    return _libs["oracle"]
+
+
+def emu_lib() -> ctypes.CDLL:
+    if "emu" not in _libs:
+        path = ROOT / "build" / "libarrow_emu.so"
+        if not path.exists():
+            _build("emu")
+        lib = ctypes.CDLL(str(path))
+        lib.arrow_emu_run.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        lib.arrow_emu_run.restype = ctypes.c_int
+        _libs["emu"] = lib
+    return _libs["emu"]
+
+
+def golden_index() -> list[dict]:
+    return json.loads((GOLDEN / "index.json").read_text())["scenarios"]
+
+
+def golden_arrays(meta: dict) -> dict:
+    with np.load(GOLDEN / meta["file"]) as z:
+        return {k: z[k] for k in z.files}
+
+
+def golden_scenario(meta: dict, arrays: dict, **overrides) -> Scenario:
+    values = dict(meta["values"])
+    values.update(overrides)
+    cfg = config_from_values(values)
+    entry = TraceEntry(arrays["arrival"], arrays["input_len"], arrays["output_len"], arrays["ids"])
+    return Scenario(entry, cfg, meta["scale"], meta["name"])
+
+
+def compile_golden(metas_arrays, validate=True):
+    scs = [golden_scenario(m, a) for m, a in metas_arrays]
+    limits = {m["stall_limit"] for m, _ in metas_arrays}
+    assert len(limits) == 1
+    return compile_batch(scs, limits.pop(), validate=validate)
+
+
+FULL = OutputSpec(requests=True, decisions=True, snapshots=True, iterlog=True, diag=True)
+
+
+def run_oracle(cb, spec=FULL, threads=1, tokens=False) -> HostBuffers:
+    spec = OutputSpec(**{**spec.__dict__, "tokens": tokens})
+    hb = HostBuffers(cb, spec)
+    b = hb.host_struct()
+    oracle_lib().pdsim_oracle_run_batch(ctypes.addressof(b), threads)
+    return hb
+
+
+def run_emu(cb, spec=FULL, width=8) -> HostBuffers:
+    hb = HostBuffers(cb, spec)
+    b = hb.host_struct()
+    rc = emu_lib().arrow_emu_run(ctypes.addressof(b), width)
+    assert rc == 0, rc
+    return hb
+
+
+def bits(x) -> np.ndarray:
+    return np.asarray(x, dtype=np.float64).view(np.uint64)
+
+
+def assert_same_f64(a, b, what):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    assert a.shape == b.shape, f"{what}: shape {a.shape} vs {b.shape}"
+    same = (bits(a) == bits(b)) | (np.isnan(a) & np.isnan(b))
+    if not same.all():
+        i = int(np.argmin(same))
+        raise AssertionError(f"{what}: first mismatch at {i}: {a[i]!r} vs {b[i]!r} ({int((~same).sum())} total)")
+
+
+def assert_same_decisions(got: np.ndarray, exp: np.ndarray, what="decisions"):
+    n = min(len(got), len(exp))
+    for k in range(n):
+        g, e = got[k], exp[k]
+        if (
+            bits(g["time"]) != bits(e["time"])
+            or int(g["request"]) != int(e["request"])
+            or int(g["instance"]) != int(e["instance"])
+            or int(g["kind"]) != int(e["kind"])
+            or int(g["code"]) != int(e["code"])
+        ):
+            raise AssertionError(f"{what}: first divergence at #{k}: got {describe(g)} expected {describe(e)}")
+    assert len(got) == len(exp), f"{what}: {len(got)} entries vs {len(exp)} expected"
+
+
+def describe(d) -> str:
+    kind = int(d["kind"])
+    if kind == 2:
+        code = int(d["code"])
+        return (f"flip t={float(d['time'])!r} inst={int(d['instance'])} {_abi.POOL_NAMES[(code >> 3) & 3]}->"
+                f"{_abi.POOL_NAMES[(code >> 5) & 3]} {_abi.TRIGGER_NAMES[code & 7]}")
+    return (f"{_abi.DECISION_KIND_NAMES[kind]} t={float(d['time'])!r} req={int(d['request'])} "
+            f"inst={int(d['instance'])} {_abi.BRANCH_NAMES[int(d['code'])]}")
+
+
+SUMMARY_KEYS = ("attainment", "p90_ttft", "p90_tpot", "mean_ttft", "mean_tpot", "goodput", "span_s")
+
+
+def check_vs_golden(meta: dict, arrays: dict, hb: HostBuffers, s: int = 0, snapshots=True) -> None:
+    """Bitwise comparison of one scenario's outputs with the reference's."""
+    summ = hb.summaries[s]
+    err = meta["error"]
+    if err is not None and err[0] == "SimulationStallError":
+        assert summ["status"] == _abi.STALLED, f"status {_abi.STATUS_NAMES[summ['status']]}, expected stall"
+        t = float(err[1].split("t=", 1)[1].split(":", 1)[0])
+        assert bits(summ["stall_time"]) == bits(t), (summ["stall_time"], t)
+        return
+    assert err is None, err
+    assert summ["status"] == _abi.OK, f"status {_abi.STATUS_NAMES[summ['status']]} overflow {summ['overflow']}"
+    assert_same_decisions(hb.decisions_of(s), arrays["decisions"])
+    sl = hb.req_slice(s)
+    assert_same_f64(hb.req_first[sl], arrays["first"], "first token")
+    assert_same_f64(hb.req_last[sl], arrays["last"], "last token")
+    exp = meta["summary"]
+    for k in SUMMARY_KEYS:
+        got = float(summ["span" if k == "span_s" else k])
+        assert bits(got) == bits(exp[k]) or (math.isinf(got) and math.isinf(exp[k])), (k, got, exp[k])
+    assert int(summ["n_ok"]) == int(((arrays["flags"] >> 2) & 1).sum())
+    assert int(summ["n_flips"]) == len(arrays["transitions"])
+    if snapshots and "snapshots" in arrays and hb.snapshots is not None:
+        got = hb.snapshots_of(s)
+        exp_s = arrays["snapshots"]
+        assert len(got) == len(exp_s), ("snapshots", len(got), len(exp_s))
+        for f in ("instance", "pool", "running_tokens", "kv_used", "queue_len", "prefill_count", "decode_count"):
+            np.testing.assert_array_equal(got[f], exp_s[f], err_msg=f"snapshot {f}")
+        for f in ("time", "pred_delay", "avg_interval"):
+            assert_same_f64(got[f], exp_s[f], f"snapshot {f}")
+
+
+def golden_free_decisions(hb: HostBuffers, s: int, cb) -> list[dict]:
+    """Decision dicts (reference format) from raw oracle outputs."""
+    from paper_2505_11916_b200 import _results
+
+    return _results.decision_dicts(hb, s, cb.table.entries[cb.trace_index[s]].ids)
