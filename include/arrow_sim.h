@@ -268,6 +268,10 @@ int arrow_sim_slots(const arrow_batch_t* batch, int* slots);
 
 const char* arrow_sim_status_string(int status);
 
+/* Sizes of the seven structs above, then every field offset in declaration
+ * order (for binding self-checks).  Returns the number of values. */
+int arrow_sim_layout(int64_t* out, int cap);
+
 #ifdef __cplusplus
 }
 #endif

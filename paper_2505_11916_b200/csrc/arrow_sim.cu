@@ -7,6 +7,7 @@
 // region of the caller's workspace (queues, rings, per-request state) sized
 // by make_layout(); traces are shared read-only by every slot.
 #include <cuda_runtime.h>
+#include <stddef.h>
 
 #include "arrow_sim.h"
 #include "sim_core.cuh"
@@ -111,6 +112,131 @@ int arrow_sim_run(const arrow_batch_t* b, void* workspace, size_t workspace_byte
     arrow_sim_kernel<1><<<grid, kThreads, 0, st>>>(*b, ws, L, counter, slots);
   return (int)cudaGetLastError();
 }
+
+// Struct sizes followed by every field offset, in declaration order, so host
+// bindings can verify their mirrors (tests/test_abi.py).  No CUDA calls.
+#define OFF(T, f) (int64_t) offsetof(T, f)
+int arrow_sim_layout(int64_t* out, int cap) {
+  const int64_t v[] = {
+    (int64_t)sizeof(arrow_scenario_t), (int64_t)sizeof(arrow_outmap_t), (int64_t)sizeof(arrow_summary_t),
+    (int64_t)sizeof(arrow_decision_t), (int64_t)sizeof(arrow_snapshot_t), (int64_t)sizeof(arrow_instdiag_t),
+    (int64_t)sizeof(arrow_batch_t),
+    OFF(arrow_scenario_t, trace_offset),
+    OFF(arrow_scenario_t, n_requests),
+    OFF(arrow_scenario_t, n_instances),
+    OFF(arrow_scenario_t, n_prefill_init),
+    OFF(arrow_scenario_t, strategy),
+    OFF(arrow_scenario_t, enable_flips),
+    OFF(arrow_scenario_t, kv_capacity),
+    OFF(arrow_scenario_t, chunk_budget),
+    OFF(arrow_scenario_t, max_batch),
+    OFF(arrow_scenario_t, bytes_per_token),
+    OFF(arrow_scenario_t, max_tokens),
+    OFF(arrow_scenario_t, stall_limit),
+    OFF(arrow_scenario_t, arrival_scale),
+    OFF(arrow_scenario_t, true_a2),
+    OFF(arrow_scenario_t, true_a1),
+    OFF(arrow_scenario_t, true_a0),
+    OFF(arrow_scenario_t, pred_a2),
+    OFF(arrow_scenario_t, pred_a1),
+    OFF(arrow_scenario_t, pred_a0),
+    OFF(arrow_scenario_t, b1),
+    OFF(arrow_scenario_t, b0),
+    OFF(arrow_scenario_t, base_latency),
+    OFF(arrow_scenario_t, bandwidth),
+    OFF(arrow_scenario_t, ttft_slo),
+    OFF(arrow_scenario_t, tpot_slo),
+    OFF(arrow_scenario_t, ttft_thr),
+    OFF(arrow_scenario_t, tpot_thr),
+    OFF(arrow_scenario_t, theta_d),
+    OFF(arrow_scenario_t, theta_busy),
+    OFF(arrow_scenario_t, breach_duration),
+    OFF(arrow_scenario_t, monitor_period),
+    OFF(arrow_scenario_t, window),
+    OFF(arrow_outmap_t, req_offset),
+    OFF(arrow_outmap_t, decision_offset),
+    OFF(arrow_outmap_t, decision_capacity),
+    OFF(arrow_outmap_t, snapshot_offset),
+    OFF(arrow_outmap_t, snapshot_capacity),
+    OFF(arrow_outmap_t, iterlog_offset),
+    OFF(arrow_outmap_t, iterlog_stride),
+    OFF(arrow_outmap_t, diag_offset),
+    OFF(arrow_outmap_t, token_offset),
+    OFF(arrow_summary_t, status),
+    OFF(arrow_summary_t, overflow),
+    OFF(arrow_summary_t, n_requests),
+    OFF(arrow_summary_t, n_completed),
+    OFF(arrow_summary_t, n_ok),
+    OFF(arrow_summary_t, n_flips),
+    OFF(arrow_summary_t, n_events),
+    OFF(arrow_summary_t, n_iterations),
+    OFF(arrow_summary_t, n_decisions),
+    OFF(arrow_summary_t, n_ticks),
+    OFF(arrow_summary_t, n_snapshots),
+    OFF(arrow_summary_t, stall_time),
+    OFF(arrow_summary_t, attainment),
+    OFF(arrow_summary_t, p90_ttft),
+    OFF(arrow_summary_t, p90_tpot),
+    OFF(arrow_summary_t, mean_ttft),
+    OFF(arrow_summary_t, mean_tpot),
+    OFF(arrow_summary_t, goodput),
+    OFF(arrow_summary_t, span),
+    OFF(arrow_summary_t, decision_hash),
+    OFF(arrow_summary_t, reserved),
+    OFF(arrow_decision_t, time),
+    OFF(arrow_decision_t, request),
+    OFF(arrow_decision_t, instance),
+    OFF(arrow_decision_t, kind),
+    OFF(arrow_decision_t, code),
+    OFF(arrow_snapshot_t, time),
+    OFF(arrow_snapshot_t, pred_delay),
+    OFF(arrow_snapshot_t, avg_interval),
+    OFF(arrow_snapshot_t, instance),
+    OFF(arrow_snapshot_t, pool),
+    OFF(arrow_snapshot_t, running_tokens),
+    OFF(arrow_snapshot_t, kv_used),
+    OFF(arrow_snapshot_t, queue_len),
+    OFF(arrow_snapshot_t, prefill_count),
+    OFF(arrow_snapshot_t, decode_count),
+    OFF(arrow_snapshot_t, reserved),
+    OFF(arrow_instdiag_t, busy_until),
+    OFF(arrow_instdiag_t, pool),
+    OFF(arrow_instdiag_t, kv_used),
+    OFF(arrow_instdiag_t, running),
+    OFF(arrow_instdiag_t, waiting),
+    OFF(arrow_instdiag_t, migrating),
+    OFF(arrow_instdiag_t, reserved),
+    OFF(arrow_batch_t, n_scenarios),
+    OFF(arrow_batch_t, flags),
+    OFF(arrow_batch_t, max_requests),
+    OFF(arrow_batch_t, max_instances),
+    OFF(arrow_batch_t, queue_capacity),
+    OFF(arrow_batch_t, emission_capacity),
+    OFF(arrow_batch_t, running_capacity),
+    OFF(arrow_batch_t, fifo_capacity),
+    OFF(arrow_batch_t, arrival),
+    OFF(arrow_batch_t, input_len),
+    OFF(arrow_batch_t, output_len),
+    OFF(arrow_batch_t, scenarios),
+    OFF(arrow_batch_t, order),
+    OFF(arrow_batch_t, outmap),
+    OFF(arrow_batch_t, summaries),
+    OFF(arrow_batch_t, req_first),
+    OFF(arrow_batch_t, req_last),
+    OFF(arrow_batch_t, req_prefill),
+    OFF(arrow_batch_t, req_decode),
+    OFF(arrow_batch_t, req_decode_iter),
+    OFF(arrow_batch_t, decisions),
+    OFF(arrow_batch_t, snapshots),
+    OFF(arrow_batch_t, iterlog),
+    OFF(arrow_batch_t, diag),
+    OFF(arrow_batch_t, token_times),
+  };
+  const int n = (int)(sizeof(v) / sizeof(v[0]));
+  for (int i = 0; i < n && i < cap; i++) out[i] = v[i];
+  return n;
+}
+#undef OFF
 
 const char* arrow_sim_status_string(int status) {
   switch (status) {

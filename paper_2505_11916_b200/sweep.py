@@ -28,3 +28,27 @@ def shard(n_items: int, rank: int, world: int) -> np.ndarray:
     """Static interleave: item i -> rank i % world (balances the rate/policy
     mix that drives per-scenario cost)."""
     return np.arange(rank, n_items, world, dtype=np.int64)
+
+
+def gather_summaries(local: np.ndarray, n_total: int, rank: int, world: int, device=None) -> np.ndarray:
+    """All-gather every rank's shard of per-scenario summaries (the sweep's
+    only collective) and return them in global scenario order.  Shards are
+    padded to equal size as collectives require."""
+    import torch
+    import torch.distributed as dist
+
+    from ._abi import SUMMARY_DTYPE
+
+    item = SUMMARY_DTYPE.itemsize
+    per = -(-n_total // world)
+    buf = torch.zeros(per * item, dtype=torch.uint8, device=device)
+    raw = np.ascontiguousarray(local).view(np.uint8).reshape(-1)
+    buf[: raw.size].copy_(torch.from_numpy(raw.copy()))
+    outs = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(outs, buf)
+    full = np.zeros(n_total, dtype=SUMMARY_DTYPE)
+    for r in range(world):
+        ids = shard(n_total, r, world)
+        data = outs[r].cpu().numpy()[: len(ids) * item]
+        full[ids] = np.frombuffer(data.tobytes(), dtype=SUMMARY_DTYPE)
+    return full

@@ -1,0 +1,87 @@
+"""The C-ABI boundary: the device library loads, exports every entry point
+include/arrow_sim.h declares, and its struct layout matches the Python
+mirrors byte for byte (no CUDA calls; runs without a GPU)."""
+
+from __future__ import annotations
+
+import ctypes
+import re
+
+import numpy as np
+import pytest
+
+import harness as H
+from paper_2505_11916_b200 import _abi
+
+LIB = H.ROOT / "paper_2505_11916_b200" / "lib" / "libarrow_sim.so"
+HEADER = H.ROOT / "include" / "arrow_sim.h"
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not LIB.exists():
+        H._build("lib")
+    return ctypes.CDLL(str(LIB))
+
+
+def declared_functions() -> list[str]:
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(arrow_sim_\w+)\s*\(", text, re.M)))
+
+
+def test_exports_every_declared_symbol(lib):
+    names = declared_functions()
+    assert {"arrow_sim_run", "arrow_sim_workspace_size", "arrow_sim_abi_version", "arrow_sim_layout"} <= set(names)
+    for name in names:
+        assert hasattr(lib, name), name
+
+
+def test_abi_version(lib):
+    lib.arrow_sim_abi_version.restype = ctypes.c_int
+    assert lib.arrow_sim_abi_version() == _abi.ABI_VERSION
+
+
+def test_struct_layout_matches_python_mirrors(lib):
+    out = (ctypes.c_int64 * 512)()
+    lib.arrow_sim_layout.restype = ctypes.c_int
+    n = lib.arrow_sim_layout(out, 512)
+    vals = list(out[:n])
+    sizes, offs = vals[:7], vals[7:]
+    dtypes = [_abi.SCENARIO_DTYPE, _abi.OUTMAP_DTYPE, _abi.SUMMARY_DTYPE, _abi.DECISION_DTYPE,
+              _abi.SNAPSHOT_DTYPE, _abi.INSTDIAG_DTYPE]
+    assert sizes == [d.itemsize for d in dtypes] + [ctypes.sizeof(_abi.Batch)]
+    expected = []
+    for d in dtypes:
+        expected += [d.fields[f][1] for f in d.names]
+    expected += [getattr(_abi.Batch, f).offset for f, _ in _abi.Batch._fields_]
+    assert offs == expected
+
+
+def test_status_strings(lib):
+    lib.arrow_sim_status_string.restype = ctypes.c_char_p
+    lib.arrow_sim_status_string.argtypes = [ctypes.c_int]
+    assert [lib.arrow_sim_status_string(i).decode() for i in range(8)] == list(_abi.STATUS_NAMES)
+
+
+def test_library_is_sm100a():
+    """The device code is built for sm_100a only (no PTX JIT fallback)."""
+    import subprocess
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", str(LIB)], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+    ptx = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-ptx", str(LIB)], capture_output=True, text=True)
+    assert ptx.stdout.strip() == ""
+
+
+def test_product_fails_loudly_without_gpu():
+    """No CPU fallback: without a CUDA device the drop-in API raises."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    import paper_2505_11916_b200 as arrow
+    from paper_2505_11916_b200._backend import EvaluatorUnavailable
+
+    trace = [arrow.TraceRequest(0, 0.0, 100, 4)]
+    with pytest.raises(EvaluatorUnavailable):
+        arrow.run(trace, arrow.default_run_config())

@@ -1,0 +1,80 @@
+"""Multi-rank sweep plumbing on CPU (gloo, world size 2): static interleaved
+sharding of a scenario sweep and the final all-gather of per-scenario
+summaries reproduce the single-process results exactly.  The CPU oracle
+stands in for the per-rank GPU launch; the gather/assembly code is the one
+bench.py uses with NCCL."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import harness as H
+from paper_2505_11916_b200 import _abi
+from paper_2505_11916_b200._buffers import OutputSpec
+from paper_2505_11916_b200.sweep import gather_summaries, shard
+
+NAMES = ["small_arrow_2_2", "small_noflip", "rr_small", "fuzz_01", "fuzz_02", "fuzz_07", "fuzz_11"]
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _items():
+    idx = {m["name"]: m for m in H.golden_index()}
+    return [(idx[n], H.golden_arrays(idx[n])) for n in NAMES]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    items = _items()
+    mine = shard(len(items), rank, world)
+    limit = {m["stall_limit"] for m, _ in items}.pop()
+    from paper_2505_11916_b200._compile import compile_batch
+
+    cb = compile_batch([H.golden_scenario(*items[i]) for i in mine], limit)
+    hb = H.run_oracle(cb, OutputSpec(), threads=1)
+    full = gather_summaries(hb.summaries, len(items), rank, world)
+    if rank == 0:
+        q.put(full.tobytes())
+    dist.destroy_process_group()
+
+
+def test_sharded_sweep_gathers_to_single_process_result():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    data = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    gathered = np.frombuffer(data, dtype=_abi.SUMMARY_DTYPE)
+    items = _items()
+    from paper_2505_11916_b200._compile import compile_batch
+
+    cb = compile_batch([H.golden_scenario(m, a) for m, a in items], items[0][0]["stall_limit"])
+    ref = H.run_oracle(cb, OutputSpec(), threads=1).summaries
+    assert gathered.tobytes() == ref.tobytes()
+    for s, (m, a) in enumerate(items):
+        assert H.bits(gathered[s]["attainment"]) == H.bits(m["summary"]["attainment"])
+
+
+def test_shard_is_a_partition():
+    for n in (1, 7, 96, 1000):
+        for world in (1, 2, 4, 8):
+            parts = np.concatenate([shard(n, r, world) for r in range(world)])
+            assert sorted(parts.tolist()) == list(range(n))
