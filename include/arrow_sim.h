@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define ARROW_SIM_ABI_VERSION 1
+#define ARROW_SIM_ABI_VERSION 2
 
 /* scheduler.py:25-28 */
 enum arrow_strategy {
@@ -145,6 +145,7 @@ typedef struct arrow_scenario {
   double breach_duration;
   double monitor_period;
   double window;                      /* interval_window_s */
+  double min_iteration;               /* lower bound on any iteration's duration (lookahead), <= 0 if none */
 } arrow_scenario_t;
 
 /* Optional per-scenario output placement; an offset < 0 disables that output. */

@@ -12,7 +12,7 @@ import ctypes
 
 import numpy as np
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # enums (include/arrow_sim.h)
 STRATEGY_CODES = {"slo-aware": 0, "minimal-load": 1, "round-robin": 2}
@@ -83,6 +83,7 @@ SCENARIO_DTYPE = np.dtype(
         ("breach_duration", np.float64),
         ("monitor_period", np.float64),
         ("window", np.float64),
+        ("min_iteration", np.float64),
     ],
     align=True,
 )

@@ -63,17 +63,24 @@ def check_device_limits(config: RunConfig) -> None:
         raise ValueError(f"kv_capacity_tokens above {KV_LIMIT} is not supported by the device evaluator")
 
 
-def emission_capacity(config: RunConfig) -> int:
-    """Upper bound on token-emitting iterations of one instance inside one
-    interval window: consecutive iterations are at least the shortest
-    possible iteration apart (b1 + b0, or a dedicated prefill of L tokens)."""
+def min_iteration(config: RunConfig) -> float:
+    """Shortest possible iteration: a token-linear batch of one token
+    (b1 + b0) or a dedicated prefill of L <= chunk budget tokens
+    (instance.py:207-212, 246-249), evaluated in the device's expression order."""
     inst = config.instance
-    dmin = inst.true_decode.b1 + inst.true_decode.b0
+    dmin = inst.true_decode.b1 * 1.0 + inst.true_decode.b0
     top = max(1, min(inst.chunk_budget, inst.kv_capacity_tokens, 1 << 20))
     L = np.arange(1, top + 1, dtype=np.float64)
     p = inst.true_prefill
     q = p.a2 * L * L + p.a1 * L + p.a0
-    dmin = min(dmin, float(q.min()))
+    return float(min(dmin, float(q.min())))
+
+
+def emission_capacity(config: RunConfig) -> int:
+    """Upper bound on token-emitting iterations of one instance inside one
+    interval window: consecutive iterations are at least the shortest
+    possible iteration apart (b1 + b0, or a dedicated prefill of L tokens)."""
+    dmin = min_iteration(config)
     if not (dmin > 0 and math.isfinite(dmin)):
         return 1 << 16
     cap = math.floor(config.interval_window_s / dmin * (1 + 1e-9)) + 3
@@ -209,6 +216,8 @@ def scenario_record(config: RunConfig, trace_offset: int, n: int, scale: float, 
     )
     rec["monitor_period"] = config.monitor_period_s
     rec["window"] = config.interval_window_s
+    dmin = min_iteration(config)
+    rec["min_iteration"] = dmin if (dmin > 0 and math.isfinite(dmin)) else 0.0
     return rec
 
 

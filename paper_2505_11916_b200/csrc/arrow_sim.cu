@@ -153,6 +153,7 @@ int arrow_sim_layout(int64_t* out, int cap) {
     OFF(arrow_scenario_t, breach_duration),
     OFF(arrow_scenario_t, monitor_period),
     OFF(arrow_scenario_t, window),
+    OFF(arrow_scenario_t, min_iteration),
     OFF(arrow_outmap_t, req_offset),
     OFF(arrow_outmap_t, decision_offset),
     OFF(arrow_outmap_t, decision_capacity),

@@ -137,6 +137,7 @@ struct Uniform {
   int64_t esp;
   int64_t n_events, n_iters, n_ticks, n_snap, n_dec;
   int64_t rr_p, rr_d;
+  int64_t n_rounds, n_serial;
   uint64_t hash;
   uint32_t seq, tick_seq;
   int a;
@@ -180,6 +181,9 @@ struct Inst {
   int rp_rid, rp_done;          // the (at most one) partially prefilled running prompt
   int wp_h, wp_c, wd_h, wd_c, mq_h, mq_c, em_h, em_c;
   int parked;
+  int min_f_cnt;                // running decodes finishing at min_f
+  int pb_pc, pb_emit;           // pending iteration pushes a PREFILL_COMPLETE / emits a token
+  int pb_rel;                   // pending iteration releases a single-token request's KV
   double dly;                   // predicted_prefill_delay at the current event
 };
 
@@ -423,13 +427,14 @@ struct Sim {
     I.em_c++;
   }
 
-  // advance_migrations, instance.py:126-146 (+ engine push, engine.py:179-181)
-  AS_HD void start_mig(Inst& I, double now) {
-    if (I.mig_active || I.mq_c == 0) return;
+  // advance_migrations, instance.py:126-146.  Returns true when a transfer
+  // starts; the caller assigns its push sequence (engine.py:179-181).
+  AS_HD bool start_mig(Inst& I, double now) {
+    if (I.mig_active || I.mq_c == 0) return false;
     int rid = mq_rid(I.id)[I.mq_h];
     int need = inl[rid] + (outl[rid] - 1);
     int kvf = sc().kv_capacity - I.kv_used - I.kv_reserved - I.committed;
-    if (kvf - I.wgrowth < need) return;
+    if (kvf - I.wgrowth < need) return false;
     I.mq_h = I.mq_h + 1 == L.qcap ? 0 : I.mq_h + 1;
     I.mq_c--;
     I.kv_reserved += inl[rid];
@@ -437,20 +442,23 @@ struct Sim {
     I.mig_rid = rid;
     const arrow_scenario_t& s = sc();
     I.mig_finish = now + (s.base_latency + (double)((int64_t)inl[rid] * s.bytes_per_token) / s.bandwidth);
-    I.mig_seq = next_seq();
+    return true;
   }
 
-  // _kick + build_iteration_batch + begin_iteration
-  // (engine.py:170-177, instance.py:175-252)
-  AS_HD void kick(Inst& I, double now) {
-    if (I.busy || !startable(I)) return;
+  // _kick + build_iteration_batch + begin_iteration (engine.py:170-177,
+  // instance.py:175-252).  Returns true when an iteration starts; the caller
+  // assigns its push sequence.  Also records whether the iteration will emit
+  // a token and whether it will push a PREFILL_COMPLETE (for the parallel
+  // rounds' quiet test).
+  AS_HD bool kick(Inst& I, double now) {
+    if (I.busy || !startable(I)) return false;
     const arrow_scenario_t& s = sc();
     const int budget = s.chunk_budget;
     const int dcap = imin(s.max_batch, budget);
     int kvf = s.kv_capacity - I.kv_used - I.kv_reserved - I.committed;
     if (I.R > dcap) {
       set_status(ARROW_INTERNAL);
-      return;
+      return false;
     }
     int nd = I.R, ad = 0;
     const int* wd = wd_rid(I.id);
@@ -464,10 +472,14 @@ struct Sim {
     }
     int rp_chunk = 0, k = 0, last_chunk = 0, last_comp = 0, ded = 0;
     int total = nd;
+    int pc = 0;                 // completing prefills with output_len > 1
+    int rel = 0;                // completing prefills with output_len == 1 (KV released)
+    int done_pf = 0;            // completing prefills
     const int* wp = wp_rid(I.id);
     bool planned = false;
     if (nd == 0 && I.rp_rid < 0 && I.wp_c > 0) {
-      int len = inl[wp[I.wp_h]];
+      int rid = wp[I.wp_h];
+      int len = inl[rid];
       if (len <= budget && len <= kvf) {
         k = 1;
         last_chunk = len;
@@ -475,6 +487,9 @@ struct Sim {
         ded = 1;
         total = len;
         planned = true;
+        done_pf = 1;
+        pc = outl[rid] > 1;
+        rel = outl[rid] == 1;
       }
     }
     if (!planned) {
@@ -493,23 +508,34 @@ struct Sim {
             left -= c;
             kvf -= c;
             total += c;
+            if (c == rem) {
+              done_pf++;
+              pc |= outl[I.rp_rid] > 1;
+              rel |= outl[I.rp_rid] == 1;
+            }
           }
         }
       }
       while (!stop && k < I.wp_c) {
         if (left <= 0) break;
-        int rem = inl[wp[ring(I.wp_h, k, L.qcap)]];
+        int rid = wp[ring(I.wp_h, k, L.qcap)];
+        int rem = inl[rid];
         int c = imin(imin(left, rem), kvf);
         if (c <= 0) break;
         k++;
         last_chunk = c;
         last_comp = c == rem;
+        if (last_comp) {
+          done_pf++;
+          pc |= outl[rid] > 1;
+          rel |= outl[rid] == 1;
+        }
         left -= c;
         kvf -= c;
         total += c;
       }
     }
-    if (nd == 0 && rp_chunk == 0 && k == 0) return;
+    if (nd == 0 && rp_chunk == 0 && k == 0) return false;
     // begin_iteration
     const int cur = I.it++;
     if (ad > 0) {
@@ -523,12 +549,17 @@ struct Sim {
         int f = cur + g - 1;
         if (I.R >= L.rcap) {
           set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_RUNNING);
-          return;
+          return false;
         }
         rr[I.R] = rid;
         rf[I.R] = f;
         I.R++;
-        if (f < I.min_f) I.min_f = f;
+        if (f < I.min_f) {
+          I.min_f = f;
+          I.min_f_cnt = 1;
+        } else if (f == I.min_f) {
+          I.min_f_cnt++;
+        }
         I.committed += g;
         I.wgrowth -= g;
         if (dit) dit[rid] = cur;
@@ -544,20 +575,24 @@ struct Sim {
     I.pb_last_chunk = last_chunk;
     I.pb_last_comp = last_comp;
     I.pb_ded = ded;
+    I.pb_pc = pc;
+    I.pb_rel = rel;
+    I.pb_emit = (nd + done_pf) > 0;
     double dur = ded ? quad(s.true_a2, s.true_a1, s.true_a0, last_chunk) : s.b1 * (double)total + s.b0;
     I.busy_until = now + dur;
     I.busy = 1;
-    I.iter_seq = next_seq();
+    return true;
   }
 
   // A prompt finished prefill: first token, park its KV, then either the
   // single-token completion or a PREFILL_COMPLETE push (engine.py:212-218).
-  AS_HD void prefill_finished(Inst& I, int rid, double now) {
+  // PREFILL_COMPLETE pushes only happen on the serial path.
+  AS_HD void prefill_finished(Inst& I, int rid, double now, int& completed) {
     p.first[rid] = now;
     if (outl[rid] == 1) {
       I.kv_used -= inl[rid];      // release_parked, instance.py:120-122
       p.last[rid] = now;
-      u().completed++;
+      completed++;
     } else {
       I.parked++;
       int c = u().fifo_count;
@@ -570,12 +605,15 @@ struct Sim {
     }
   }
 
-  // ITERATION_COMPLETE on the owner lane: execute_iteration + the engine
-  // handler (instance.py:254-288, engine.py:205-223).  Returns the drained
-  // pool move to perform (-1 none) as dst pool.
-  AS_HD int iteration_complete(Inst& I, double now) {
+  // ITERATION_COMPLETE for one instance: execute_iteration + the engine
+  // handler (instance.py:254-288, engine.py:205-223).  Touches only this
+  // instance's state and per-request outputs, except (SERIAL only) the
+  // PREFILL_COMPLETE FIFO and the push sequence.  Adds finished requests to
+  // `completed`; returns the drained-pool move (-1 none); sets `pushed` when
+  // the next iteration started (its sequence is assigned here if SERIAL).
+  template <bool SERIAL>
+  AS_HD int iteration_complete(Inst& I, double now, int& completed, bool& pushed) {
     const int cur = I.it - 1;
-    u().n_iters++;
     if (B->iterlog && have_om && om.iterlog_offset >= 0) {
       if (cur < om.iterlog_stride)
         B->iterlog[om.iterlog_offset + (int64_t)I.id * om.iterlog_stride + cur] = now;
@@ -583,7 +621,7 @@ struct Sim {
         u().overflow = ARROW_OVF_ITERLOG;
     }
     const int nd = I.pb_ndec;
-    int nfin = 0, npf = 0;
+    int npf = 0;
     if (nd > 0) {
       I.kv_used += nd;
       I.committed -= nd;
@@ -591,7 +629,7 @@ struct Sim {
       if (I.min_f == cur) {
         int* rr = run_rid(I.id);
         int* rf = run_f(I.id);
-        int m = 0x7fffffff;
+        int m = 0x7fffffff, mc = 0;
         int j = 0;
         while (j < I.R) {
           int f = rf[j];
@@ -601,16 +639,22 @@ struct Sim {
             I.kv_used -= held;
             I.rtok -= held;
             p.last[rid] = now;
-            nfin++;
+            completed++;
             I.R--;
             rr[j] = rr[I.R];
             rf[j] = rf[I.R];
           } else {
-            if (f < m) m = f;
+            if (f < m) {
+              m = f;
+              mc = 1;
+            } else if (f == m) {
+              mc++;
+            }
             j++;
           }
         }
         I.min_f = m;
+        I.min_f_cnt = mc;
       }
     }
     if (I.pb_rp_chunk > 0) {
@@ -619,7 +663,7 @@ struct Sim {
         int rid = I.rp_rid;
         I.rp_rid = -1;
         npf++;
-        prefill_finished(I, rid, now);
+        prefill_finished(I, rid, now, completed);
       }
     }
     if (I.pb_k > 0) {
@@ -628,7 +672,7 @@ struct Sim {
         int rid = wp[ring(I.wp_h, j, L.qcap)];
         if (j < I.pb_k - 1 || I.pb_last_comp) {
           npf++;
-          prefill_finished(I, rid, now);
+          prefill_finished(I, rid, now, completed);
         } else {
           I.rp_rid = rid;
           I.rp_done = I.pb_last_chunk;
@@ -639,11 +683,7 @@ struct Sim {
     }
     I.busy = 0;
     I.pb_ndec = I.pb_rp_chunk = I.pb_k = I.pb_last_chunk = I.pb_last_comp = I.pb_ded = 0;
-    if (nd + npf > 0) {
-      emit(I, now);
-      u().esp = 0;
-    }
-    u().completed += nfin;
+    if (nd + npf > 0) emit(I, now);
     // _check_drained (engine.py:183-192): decided here, applied by the warp
     int dst = -1;
     int pk = pool_of(I.id);
@@ -651,8 +691,14 @@ struct Sim {
       dst = P_DECODE;
     else if (pk == P_D2P && !has_decode_work(I))
       dst = P_PREFILL;
-    start_mig(I, now);
-    kick(I, now);
+    if (SERIAL) {
+      if (nd + npf > 0) u().esp = 0;
+      if (start_mig(I, now)) I.mig_seq = next_seq();
+      pushed = kick(I, now);
+      if (pushed) I.iter_seq = next_seq();
+    } else {
+      pushed = kick(I, now);
+    }
     return dst;
   }
 
@@ -990,7 +1036,7 @@ struct Sim {
       wp_rid(I.id)[slot] = rid;
       wp_term(I.id)[slot] = own;
       I.wp_c++;
-      kick(I, now);
+      if (kick(I, now)) I.iter_seq = next_seq();
     });
   }
 
@@ -1020,8 +1066,8 @@ struct Sim {
         }
         mq_rid(I.id)[ring(I.mq_h, I.mq_c, L.qcap)] = rid;
         I.mq_c++;
-        start_mig(I, now);
-        kick(I, now);
+        if (start_mig(I, now)) I.mig_seq = next_seq();
+        if (kick(I, now)) I.iter_seq = next_seq();
         return;
       }
       if (I.wd_c >= L.qcap) {
@@ -1032,7 +1078,7 @@ struct Sim {
       I.wd_c++;
       I.wgrowth += g;
       I.rtok += in;
-      kick(I, now);
+      if (kick(I, now)) I.iter_seq = next_seq();
     });
   }
 
@@ -1060,10 +1106,18 @@ struct Sim {
       S.kv_used -= inl[rid];   // release_parked
       S.parked--;
     });
-    owner(id, [&](Inst& I) { start_mig(I, now); });
-    owner(src, [&](Inst& S) { start_mig(S, now); });
-    owner(id, [&](Inst& I) { kick(I, now); });
-    owner(src, [&](Inst& S) { kick(S, now); });
+    owner(id, [&](Inst& I) {
+      if (start_mig(I, now)) I.mig_seq = next_seq();
+    });
+    owner(src, [&](Inst& S) {
+      if (start_mig(S, now)) S.mig_seq = next_seq();
+    });
+    owner(id, [&](Inst& I) {
+      if (kick(I, now)) I.iter_seq = next_seq();
+    });
+    owner(src, [&](Inst& S) {
+      if (kick(S, now)) S.iter_seq = next_seq();
+    });
   }
 
   AS_HD void write_snapshots(double now) {
@@ -1215,15 +1269,52 @@ struct Sim {
     w.sync();
   }
 
-  // Next event: lexicographic (time, kind, seq) minimum over every pending
-  // event (engine.py:267).  Returns the event code: 2*inst + kind for
-  // instance events, 1000 + kind for global ones, -1 when the heap is empty.
-  AS_HD int next_event(double* when) {
+  // Event selection (engine.py:267: pop the lexicographic (time, kind, seq)
+  // minimum).  Pending events are split into
+  //   * serial events: arrivals, PREFILL_COMPLETE, monitor ticks, migration
+  //     completions, and "loud" iteration completions (those that push a
+  //     PREFILL_COMPLETE, may start a migration, may drain a transition-pool
+  //     instance, or emit nothing);
+  //   * quiet iteration completions, whose handler touches only their own
+  //     instance.
+  // Let H be the earliest serial event.  Every quiet event before H whose
+  // time is <= T = min_i(t_i + dl_i) over those quiet events (dl_i a lower
+  // bound on the duration of the iteration instance i will start next) can be
+  // executed in one round, lane-parallel: all of them precede every event the
+  // round creates and every serial event, so the global order is preserved;
+  // the round's pushes get their exact global sequence numbers by ranking the
+  // round's events by (time, seq).  Returns:
+  //   -1 nothing pending; kRound for a parallel round (part[] set per slot);
+  //   otherwise a serial event code (2*inst + kind, or 1000 + kind).
+  static constexpr int kRound = 5000;
+
+  // A queued migration can only start at this completion if the iteration
+  // frees KV: X = kv_free - waiting growth never increases between
+  // handlers without a start_mig attempt (instance.py:140 gate failed at a
+  // state >= the current one), and executing an iteration changes X only by
+  // finished decodes and released single-token prompts.
+  AS_HD bool quiet(const Inst& I) const {
+    const int pk = pool_of(I.id);
+    const bool frees = I.min_f == I.it - 1 || I.pb_rel;
+    return I.busy && I.pb_emit && !I.pb_pc && (pk == P_PREFILL || pk == P_DECODE) &&
+           !(I.mq_c > 0 && !I.mig_active && frees);
+  }
+
+  // Lower bound on the duration of the iteration this instance starts when
+  // its pending iteration completes: its surviving running decodes are all
+  // in the next batch (token-linear cost), otherwise the scenario minimum.
+  AS_HD double next_duration_bound(const Inst& I) const {
+    const int cur = I.it - 1;
+    const int r_next = I.R - (I.min_f == cur ? I.min_f_cnt : 0);
+    if (r_next >= 1) return sc().b1 * (double)r_next + sc().b0;
+    return sc().min_iteration;
+  }
+
+  AS_HD int select_events(double* when, bool part[IPL]) {
     uint64_t bk = ~0ull;
     uint32_t bs = ~0u;
     int code = -1;
-    auto offer = [&](double t, int kind, uint32_t seq, int c) {
-      uint64_t k1 = okey(t);
+    auto offer = [&](uint64_t k1, int kind, uint32_t seq, int c) {
       uint32_t k2 = ((uint32_t)kind << 28) | seq;
       if (code < 0 || k1 < bk || (k1 == bk && k2 < bs)) {
         bk = k1;
@@ -1231,23 +1322,124 @@ struct Sim {
         code = c;
       }
     };
+    bool q[IPL];
+    uint64_t qk[IPL];
 #pragma unroll
     for (int k = 0; k < IPL; k++) {
       const Inst& I = st[k];
+      q[k] = false;
+      qk[k] = 0;
+      part[k] = false;
       if (I.id < 0) continue;
-      if (I.busy) offer(I.busy_until, EV_ITER, I.iter_seq, 2 * I.id + 1);
-      if (I.mig_active) offer(I.mig_finish, EV_MIG, I.mig_seq, 2 * I.id);
+      if (I.busy) {
+        uint64_t k1 = okey(I.busy_until);
+        if (quiet(I)) {
+          q[k] = true;
+          qk[k] = k1;
+        } else {
+          offer(k1, EV_ITER, I.iter_seq, 2 * I.id + 1);
+        }
+      }
+      if (I.mig_active) offer(okey(I.mig_finish), EV_MIG, I.mig_seq, 2 * I.id);
     }
     if (lane == 0) {
       const Uniform& U = sm->u;
-      if (U.a < sc().n_requests) offer(U.next_arrival, EV_ARRIVAL, (uint32_t)U.a, 1000 + EV_ARRIVAL);
-      if (U.fifo_count > 0) offer(p.fifo_time[U.fifo_head], EV_PREFILL, p.fifo_seq[U.fifo_head], 1000 + EV_PREFILL);
-      if (U.tick_active) offer(U.tick_time, EV_TICK, U.tick_seq, 1000 + EV_TICK);
+      if (U.a < sc().n_requests) offer(okey(U.next_arrival), EV_ARRIVAL, (uint32_t)U.a, 1000 + EV_ARRIVAL);
+      if (U.fifo_count > 0)
+        offer(okey(p.fifo_time[U.fifo_head]), EV_PREFILL, p.fifo_seq[U.fifo_head], 1000 + EV_PREFILL);
+      if (U.tick_active) offer(okey(U.tick_time), EV_TICK, U.tick_seq, 1000 + EV_TICK);
     }
-    int wl = warp_argmin(bk, bs, code >= 0);
-    if (wl < 0) return -1;
-    *when = okey_inv(w.shfl(bk, wl));
-    return w.shfl(code, wl);
+    const int wl = warp_argmin(bk, bs, code >= 0);
+    uint64_t hk = ~0ull;
+    uint32_t hs = ~0u;
+    if (wl >= 0) {
+      hk = w.shfl(bk, wl);
+      hs = w.shfl(bs, wl);
+    }
+    bool cand[IPL];
+    bool any_cand = false;
+    uint64_t lim = ~0ull;
+#pragma unroll
+    for (int k = 0; k < IPL; k++) {
+      const uint32_t k2 = ((uint32_t)EV_ITER << 28) | st[k].iter_seq;
+      cand[k] = q[k] && (qk[k] < hk || (qk[k] == hk && k2 < hs));
+      if (cand[k]) {
+        any_cand = true;
+        uint64_t x = okey(st[k].busy_until + next_duration_bound(st[k]));
+        if (x < lim) lim = x;
+      }
+    }
+    if (!w.any(any_cand)) {
+      if (wl < 0) return -1;
+      *when = okey_inv(hk);
+      return w.shfl(code, wl);
+    }
+    uint32_t hi = w.min_u32((uint32_t)(lim >> 32));
+    uint32_t lo = w.min_u32((uint32_t)(lim >> 32) == hi ? (uint32_t)lim : ~0u);
+    const uint64_t cut = ((uint64_t)hi << 32) | lo;
+#pragma unroll
+    for (int k = 0; k < IPL; k++) part[k] = cand[k] && qk[k] <= cut;
+    return kRound;
+  }
+
+  // One parallel round of quiet iteration completions.
+  AS_HD void run_round(const bool part[IPL]) {
+    uint64_t key1[IPL];
+    uint32_t key2[IPL];
+    bool pushed[IPL];
+    int completed = 0, n_part = 0;
+#pragma unroll
+    for (int k = 0; k < IPL; k++) {
+      pushed[k] = false;
+      key1[k] = 0;
+      key2[k] = 0;
+      if (!part[k]) continue;
+      Inst& I = st[k];
+      key1[k] = okey(I.busy_until);
+      key2[k] = I.iter_seq;
+      n_part++;
+      iteration_complete<false>(I, I.busy_until, completed, pushed[k]);
+    }
+    // exact push sequence: the round's pushes, in (time, seq) order of the
+    // events that made them, continue the global counter
+    const uint32_t base = u().seq;
+    int pre[IPL];
+#pragma unroll
+    for (int k = 0; k < IPL; k++) pre[k] = 0;
+    int my_push = 0;
+#pragma unroll
+    for (int kk = 0; kk < IPL; kk++) {
+      uint32_t m = w.ballot(pushed[kk]);
+      while (m) {
+        const int j = ffs32(m);
+        m &= m - 1;
+        const uint64_t a = w.shfl(key1[kk], j);
+        const uint32_t b = w.shfl(key2[kk], j);
+#pragma unroll
+        for (int k = 0; k < IPL; k++)
+          if (pushed[k] && (a < key1[k] || (a == key1[k] && b < key2[k]))) pre[k]++;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < IPL; k++)
+      if (pushed[k]) {
+        st[k].iter_seq = base + (uint32_t)pre[k];
+        my_push++;
+      }
+    const uint32_t total_push = w.add_u32((uint32_t)my_push);
+    const uint32_t total_part = w.add_u32((uint32_t)n_part);
+    const uint32_t total_done = w.add_u32((uint32_t)completed);
+    w.sync();
+    lane0([&] {
+      Uniform& U = u();
+      if (base + total_push >= SEQ_LIMIT) set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_SEQ);
+      U.seq = base + total_push;
+      U.esp = 0;  // every quiet event emits a token
+      U.n_events += total_part;
+      U.n_iters += total_part;
+      U.n_rounds++;
+      U.completed += (int)total_done;
+    });
   }
 
   AS_HD bool only_tick_pending() {
@@ -1264,12 +1456,21 @@ struct Sim {
     for (;;) {
       w.sync();
       double now = 0.0;
-      int ev = next_event(&now);
+      bool part[IPL];
+      int ev = select_events(&now, part);
       if (ev < 0) break;
+      if (ev == kRound) {
+        run_round(part);
+        const int status = u().status;
+        w.sync();
+        if (status != ARROW_OK) return;
+        continue;
+      }
       lane0([&] {
         u().now = now;
         u().esp++;
         u().n_events++;
+        u().n_serial++;
         ATRACE("ev %d t=%.17g esp=%lld\n", ev, now, (long long)u().esp);
       });
       if (ev >= 1000) {
@@ -1316,7 +1517,13 @@ struct Sim {
         int id = ev >> 1;
         if (ev & 1) {
           int dst = -1;
-          owner(id, [&](Inst& I) { u().tmp_i[0] = iteration_complete(I, now); });
+          owner(id, [&](Inst& I) {
+            int completed = 0;
+            bool pushed = false;
+            u().n_iters++;
+            u().tmp_i[0] = iteration_complete<true>(I, now, completed, pushed);
+            u().completed += completed;
+          });
           dst = u().tmp_i[0];
           w.sync();
           if (dst >= 0) move_and_log(id, dst, now, ARROW_TRIG_DRAINED);
@@ -1481,6 +1688,8 @@ struct Sim {
       out->n_snapshots = U.n_snap;
       out->stall_time = U.status == ARROW_STALLED ? U.stall_time : NAN;
       out->decision_hash = U.hash;
+      out->reserved[0] = U.n_serial;   // serial (one-event) steps
+      out->reserved[1] = U.n_rounds;   // lane-parallel rounds
       out->attainment = out->p90_ttft = out->p90_tpot = NAN;
       out->mean_ttft = out->mean_tpot = out->goodput = out->span = NAN;
     }
