@@ -38,8 +38,7 @@ def _build(target: str) -> None:
 def oracle_lib() -> ctypes.CDLL:
     if "oracle" not in _libs:
         path = ROOT / "oracle" / "build" / "libpdsim_oracle.so"
-        if not path.exists():
-            _build("oracle")
+        _build("oracle")          # incremental: rebuilds when the shared header changed
         lib = ctypes.CDLL(str(path))
         lib.pdsim_oracle_run_batch.argtypes = [ctypes.c_void_p, ctypes.c_int]
         lib.pdsim_oracle_run_batch.restype = ctypes.c_int
@@ -54,8 +53,7 @@ def oracle_lib() -> ctypes.CDLL:
 def emu_lib() -> ctypes.CDLL:
     if "emu" not in _libs:
         path = ROOT / "build" / "libarrow_emu.so"
-        if not path.exists():
-            _build("emu")
+        _build("emu")
         lib = ctypes.CDLL(str(path))
         lib.arrow_emu_run.argtypes = [ctypes.c_void_p, ctypes.c_int]
         lib.arrow_emu_run.restype = ctypes.c_int
