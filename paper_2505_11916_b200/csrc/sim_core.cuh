@@ -184,6 +184,8 @@ struct Inst {
   int min_f_cnt;                // running decodes finishing at min_f
   int pb_pc, pb_emit;           // pending iteration pushes a PREFILL_COMPLETE / emits a token
   int pb_rel;                   // pending iteration releases a single-token request's KV
+  int cq;                       // cached: pending iteration is quiet
+  uint64_t ck;                  // cached: order key of busy_until
   double dly;                   // predicted_prefill_delay at the current event
 };
 
@@ -395,33 +397,42 @@ struct Sim {
     return d;
   }
 
-  // avg_token_interval, instance.py:323-329.  The ring keeps only emissions
-  // still inside some future query window; cursors only move forward
-  // because simulated time is monotone.
+  // avg_token_interval, instance.py:323-329: over emissions with
+  // t >= now - window.  The ring holds this instance's emission times in
+  // increasing order; entries older than any future query window are
+  // dropped lazily (here, by binary search, and when the ring fills), which
+  // is exact because query times never decrease.
   AS_HD bool interval(Inst& I, double now, double* out) {
-    double lo = now - sc().window;
-    double* e = em(I.id);
-    while (I.em_c > 0 && e[I.em_h] < lo) {
-      I.em_h = I.em_h + 1 == L.ecap ? 0 : I.em_h + 1;
-      I.em_c--;
+    const double lo = now - sc().window;
+    const double* e = em(I.id);
+    if (I.em_c > 0 && e[I.em_h] < lo) {
+      int a = 0, b = I.em_c;          // first offset with t >= lo lies in (a, b]
+      while (b - a > 1) {
+        int mid = (a + b) >> 1;
+        if (e[ring(I.em_h, mid, L.ecap)] < lo)
+          a = mid;
+        else
+          b = mid;
+      }
+      I.em_h = ring(I.em_h, b, L.ecap);
+      I.em_c -= b;
     }
     if (I.em_c < 2) return false;
-    double first = e[I.em_h];
-    double last = e[ring(I.em_h, I.em_c - 1, L.ecap)];
+    const double first = e[I.em_h];
+    const double last = e[ring(I.em_h, I.em_c - 1, L.ecap)];
     *out = (last - first) / (double)(I.em_c - 1);
     return true;
   }
 
   AS_HD void emit(Inst& I, double now) {
-    double lo = now - sc().window;
     double* e = em(I.id);
-    while (I.em_c > 0 && e[I.em_h] < lo) {
-      I.em_h = I.em_h + 1 == L.ecap ? 0 : I.em_h + 1;
-      I.em_c--;
-    }
     if (I.em_c >= L.ecap) {
-      set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_EMISSION);
-      return;
+      double v;
+      interval(I, now, &v);             // drops everything outside the window
+      if (I.em_c >= L.ecap) {
+        set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_EMISSION);
+        return;
+      }
     }
     e[ring(I.em_h, I.em_c, L.ecap)] = now;
     I.em_c++;
@@ -1284,9 +1295,6 @@ struct Sim {
   // round creates and every serial event, so the global order is preserved;
   // the round's pushes get their exact global sequence numbers by ranking the
   // round's events by (time, seq).  Returns:
-  //   -1 nothing pending; kRound for a parallel round (part[] set per slot);
-  //   otherwise a serial event code (2*inst + kind, or 1000 + kind).
-  static constexpr int kRound = 5000;
 
   // A queued migration can only start at this completion if the iteration
   // frees KV: X = kv_free - waiting growth never increases between
@@ -1310,80 +1318,98 @@ struct Sim {
     return sc().min_iteration;
   }
 
-  AS_HD int select_events(double* when, bool part[IPL]) {
-    uint64_t bk = ~0ull;
-    uint32_t bs = ~0u;
-    int code = -1;
-    auto offer = [&](uint64_t k1, int kind, uint32_t seq, int c) {
-      uint32_t k2 = ((uint32_t)kind << 28) | seq;
-      if (code < 0 || k1 < bk || (k1 == bk && k2 < bs)) {
-        bk = k1;
-        bs = k2;
-        code = c;
-      }
-    };
-    bool q[IPL];
-    uint64_t qk[IPL];
+  // The earliest serial event (time key, kind|seq, code); code -1 = none.
+  struct Head {
+    uint64_t k;
+    uint32_t s;
+    int code;
+  };
+
+  AS_HD void offer(Head& h, uint64_t k1, int kind, uint32_t seq, int c) const {
+    const uint32_t k2 = ((uint32_t)kind << 28) | seq;
+    if (h.code < 0 || k1 < h.k || (k1 == h.k && k2 < h.s)) {
+      h.k = k1;
+      h.s = k2;
+      h.code = c;
+    }
+  }
+
+  AS_HD void classify(Inst& I) const {
+    I.ck = okey(I.busy_until);
+    I.cq = quiet(I) ? 1 : 0;
+  }
+
+  // Warp-uniform minimum of per-lane heads.
+  AS_HD Head reduce_head(const Head& mine) {
+    Head h;
+    h.code = -1;
+    h.k = ~0ull;
+    h.s = ~0u;
+    const int wl = warp_argmin(mine.k, mine.s, mine.code >= 0);
+    if (wl >= 0) {
+      h.k = w.shfl(mine.k, wl);
+      h.s = w.shfl(mine.s, wl);
+      h.code = w.shfl(mine.code, wl);
+    }
+    return h;
+  }
+
+  // Full rescan after a serial step: classify every pending iteration and
+  // find the earliest serial event (lane 0 adds arrival, FIFO head, tick).
+  AS_HD Head full_scan() {
+    Head mine;
+    mine.code = -1;
+    mine.k = ~0ull;
+    mine.s = ~0u;
 #pragma unroll
     for (int k = 0; k < IPL; k++) {
-      const Inst& I = st[k];
-      q[k] = false;
-      qk[k] = 0;
-      part[k] = false;
+      Inst& I = st[k];
       if (I.id < 0) continue;
       if (I.busy) {
-        uint64_t k1 = okey(I.busy_until);
-        if (quiet(I)) {
-          q[k] = true;
-          qk[k] = k1;
-        } else {
-          offer(k1, EV_ITER, I.iter_seq, 2 * I.id + 1);
-        }
+        classify(I);
+        if (!I.cq) offer(mine, I.ck, EV_ITER, I.iter_seq, 2 * I.id + 1);
       }
-      if (I.mig_active) offer(okey(I.mig_finish), EV_MIG, I.mig_seq, 2 * I.id);
+      if (I.mig_active) offer(mine, okey(I.mig_finish), EV_MIG, I.mig_seq, 2 * I.id);
     }
     if (lane == 0) {
       const Uniform& U = sm->u;
-      if (U.a < sc().n_requests) offer(okey(U.next_arrival), EV_ARRIVAL, (uint32_t)U.a, 1000 + EV_ARRIVAL);
+      if (U.a < sc().n_requests) offer(mine, okey(U.next_arrival), EV_ARRIVAL, (uint32_t)U.a, 1000 + EV_ARRIVAL);
       if (U.fifo_count > 0)
-        offer(okey(p.fifo_time[U.fifo_head]), EV_PREFILL, p.fifo_seq[U.fifo_head], 1000 + EV_PREFILL);
-      if (U.tick_active) offer(okey(U.tick_time), EV_TICK, U.tick_seq, 1000 + EV_TICK);
+        offer(mine, okey(p.fifo_time[U.fifo_head]), EV_PREFILL, p.fifo_seq[U.fifo_head], 1000 + EV_PREFILL);
+      if (U.tick_active) offer(mine, okey(U.tick_time), EV_TICK, U.tick_seq, 1000 + EV_TICK);
     }
-    const int wl = warp_argmin(bk, bs, code >= 0);
-    uint64_t hk = ~0ull;
-    uint32_t hs = ~0u;
-    if (wl >= 0) {
-      hk = w.shfl(bk, wl);
-      hs = w.shfl(bs, wl);
-    }
-    bool cand[IPL];
+    return reduce_head(mine);
+  }
+
+  // Quiet events before the head whose times are <= T = min(t_i + dl_i):
+  // one lane-parallel round.  Returns false when none qualifies.
+  AS_HD bool round_select(const Head& h, bool part[IPL]) {
     bool any_cand = false;
     uint64_t lim = ~0ull;
+    bool cand[IPL];
 #pragma unroll
     for (int k = 0; k < IPL; k++) {
-      const uint32_t k2 = ((uint32_t)EV_ITER << 28) | st[k].iter_seq;
-      cand[k] = q[k] && (qk[k] < hk || (qk[k] == hk && k2 < hs));
+      const Inst& I = st[k];
+      const uint32_t k2 = ((uint32_t)EV_ITER << 28) | I.iter_seq;
+      cand[k] = I.id >= 0 && I.busy && I.cq && (h.code < 0 || I.ck < h.k || (I.ck == h.k && k2 < h.s));
       if (cand[k]) {
         any_cand = true;
-        uint64_t x = okey(st[k].busy_until + next_duration_bound(st[k]));
+        const uint64_t x = okey(I.busy_until + next_duration_bound(I));
         if (x < lim) lim = x;
       }
     }
-    if (!w.any(any_cand)) {
-      if (wl < 0) return -1;
-      *when = okey_inv(hk);
-      return w.shfl(code, wl);
-    }
-    uint32_t hi = w.min_u32((uint32_t)(lim >> 32));
-    uint32_t lo = w.min_u32((uint32_t)(lim >> 32) == hi ? (uint32_t)lim : ~0u);
+    if (!w.any(any_cand)) return false;
+    const uint32_t hi = w.min_u32((uint32_t)(lim >> 32));
+    const uint32_t lo = w.min_u32((uint32_t)(lim >> 32) == hi ? (uint32_t)lim : ~0u);
     const uint64_t cut = ((uint64_t)hi << 32) | lo;
 #pragma unroll
-    for (int k = 0; k < IPL; k++) part[k] = cand[k] && qk[k] <= cut;
-    return kRound;
+    for (int k = 0; k < IPL; k++) part[k] = cand[k] && st[k].ck <= cut;
+    return true;
   }
 
-  // One parallel round of quiet iteration completions.
-  AS_HD void run_round(const bool part[IPL]) {
+  // One parallel round of quiet iteration completions; folds any loud
+  // event the round created into the head.
+  AS_HD void run_round(const bool part[IPL], Head& h) {
     uint64_t key1[IPL];
     uint32_t key2[IPL];
     bool pushed[IPL];
@@ -1420,15 +1446,28 @@ struct Sim {
           if (pushed[k] && (a < key1[k] || (a == key1[k] && b < key2[k]))) pre[k]++;
       }
     }
+    Head loud;
+    loud.code = -1;
+    loud.k = ~0ull;
+    loud.s = ~0u;
 #pragma unroll
     for (int k = 0; k < IPL; k++)
       if (pushed[k]) {
-        st[k].iter_seq = base + (uint32_t)pre[k];
+        Inst& I = st[k];
+        I.iter_seq = base + (uint32_t)pre[k];
         my_push++;
+        classify(I);
+        if (!I.cq) offer(loud, I.ck, EV_ITER, I.iter_seq, 2 * I.id + 1);
       }
-    const uint32_t total_push = w.add_u32((uint32_t)my_push);
-    const uint32_t total_part = w.add_u32((uint32_t)n_part);
-    const uint32_t total_done = w.add_u32((uint32_t)completed);
+    if (w.any(loud.code >= 0)) {
+      Head nl = reduce_head(loud);
+      if (h.code < 0 || nl.k < h.k || (nl.k == h.k && nl.s < h.s)) h = nl;
+    }
+    // one reduction: pushes (<= 64) | participants (<= 64) << 7 | finished requests << 14
+    const uint32_t packed = w.add_u32((uint32_t)my_push | ((uint32_t)n_part << 7) | ((uint32_t)completed << 14));
+    const uint32_t total_push = packed & 127u;
+    const uint32_t total_part = (packed >> 7) & 127u;
+    const uint32_t total_done = packed >> 14;
     w.sync();
     lane0([&] {
       Uniform& U = u();
@@ -1453,19 +1492,19 @@ struct Sim {
 
   AS_HD void simulate() {
     const int64_t limit = sc().stall_limit;
+    Head h = full_scan();
     for (;;) {
-      w.sync();
-      double now = 0.0;
       bool part[IPL];
-      int ev = select_events(&now, part);
-      if (ev < 0) break;
-      if (ev == kRound) {
-        run_round(part);
+      if (round_select(h, part)) {
+        run_round(part, h);
         const int status = u().status;
         w.sync();
         if (status != ARROW_OK) return;
         continue;
       }
+      if (h.code < 0) break;
+      const int ev = h.code;
+      double now = okey_inv(h.k);
       lane0([&] {
         u().now = now;
         u().esp++;
@@ -1542,6 +1581,7 @@ struct Sim {
         });
         return;
       }
+      h = full_scan();
     }
     // end-of-run checks, engine.py:286-290
     const int completed = u().completed;
