@@ -252,6 +252,9 @@ def run_ours(args, rank: int, world: int) -> None:
     hb = db.download(["summaries"])
     torch.cuda.synchronize(dev)
     statuses = np.bincount(hb.summaries["status"], minlength=8)
+    dump = os.environ.get("ARROW_BENCH_DUMP")
+    if dump and rank == 0:
+        np.save(dump, hb.summaries)
 
     # e2e through the public API: compile + pinned H2D + kernel + D2H summaries
     e2e_times = []

@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define ARROW_SIM_ABI_VERSION 2
+#define ARROW_SIM_ABI_VERSION 3
 
 /* scheduler.py:25-28 */
 enum arrow_strategy {
@@ -183,7 +183,10 @@ typedef struct arrow_summary {
   double goodput;
   double span;
   uint64_t decision_hash;     /* FNV-1a over the decision stream */
-  int64_t reserved[2];
+  int64_t n_serial_steps;     /* evaluator: events executed one at a time */
+  int64_t n_parallel_steps;   /* evaluator: lane-parallel rounds + chain bursts */
+  int64_t cycles;             /* evaluator: SM clock cycles spent on this scenario */
+  int64_t reserved;
 } arrow_summary_t;
 
 /* One entry of GlobalScheduler.decisions (scheduler.py:104-122). */

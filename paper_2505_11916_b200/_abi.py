@@ -12,7 +12,7 @@ import ctypes
 
 import numpy as np
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 # enums (include/arrow_sim.h)
 STRATEGY_CODES = {"slo-aware": 0, "minimal-load": 1, "round-robin": 2}
@@ -125,7 +125,10 @@ SUMMARY_DTYPE = np.dtype(
         ("goodput", np.float64),
         ("span", np.float64),
         ("decision_hash", np.uint64),
-        ("reserved", np.int64, (2,)),
+        ("n_serial_steps", np.int64),
+        ("n_parallel_steps", np.int64),
+        ("cycles", np.int64),
+        ("reserved", np.int64),
     ],
     align=True,
 )

@@ -183,6 +183,9 @@ int arrow_sim_layout(int64_t* out, int cap) {
     OFF(arrow_summary_t, goodput),
     OFF(arrow_summary_t, span),
     OFF(arrow_summary_t, decision_hash),
+    OFF(arrow_summary_t, n_serial_steps),
+    OFF(arrow_summary_t, n_parallel_steps),
+    OFF(arrow_summary_t, cycles),
     OFF(arrow_summary_t, reserved),
     OFF(arrow_decision_t, time),
     OFF(arrow_decision_t, request),

@@ -54,6 +54,8 @@ enum { EV_MIG = 0, EV_ITER = 1, EV_PREFILL = 2, EV_ARRIVAL = 3, EV_TICK = 4 };
 enum { P_PREFILL = 0, P_DECODE = 1, P_P2D = 2, P_D2P = 3 };
 static constexpr int MAX_INST = 64;
 static constexpr uint32_t SEQ_LIMIT = 1u << 28;
+static constexpr int BURST_POOL = 512;  // chain-burst event keys per warp (shared memory)
+static constexpr int BURST_MAX = 64;    // events per instance per chain burst
 
 // ---------------------------------------------------------------- layout --
 
@@ -137,7 +139,7 @@ struct Uniform {
   int64_t esp;
   int64_t n_events, n_iters, n_ticks, n_snap, n_dec;
   int64_t rr_p, rr_d;
-  int64_t n_rounds, n_serial;
+  int64_t n_rounds, n_serial, n_bursts;
   uint64_t hash;
   uint32_t seq, tick_seq;
   int a;
@@ -159,6 +161,13 @@ struct WarpSmem {
   double vals[MAX_INST];
   int valid[MAX_INST];
   int hist[256];
+  uint64_t blist[BURST_POOL];    // chain-burst event keys, one segment per instance
+  int bcount[MAX_INST];          // events each instance ran in the current burst
+  int boff[MAX_INST];            // its segment in blist
+  int bhead[MAX_INST];           // merge cursor (tie fallback)
+  int blast[MAX_INST];           // its last event pushed a successor
+  uint32_t bseq[MAX_INST];       // sequence of its head / final pending push
+  int btie;
 };
 
 // Registers of one instance on its owner lane (instance.py:78-92, reshaped).
@@ -1481,6 +1490,350 @@ struct Sim {
     });
   }
 
+  // ---------------------------------------------------- chain bursts ----
+  //
+  // An instance with no prefill work and no queued migration, in a non-
+  // transition pool, can only run decode-only iterations until the next
+  // serial event: every one of them emits tokens, pushes nothing but its
+  // successor and touches nothing but its own state.  Such "chain-safe"
+  // instances run their event chains in a local loop up to a horizon that
+  // precedes every other pending event, then a merge of the per-instance
+  // event lists (by time, ties by sequence) assigns the exact global push
+  // sequence numbers the serial order would have produced.
+
+  AS_HD bool chain_safe(const Inst& I) const {
+    return I.busy && I.cq && I.rp_rid < 0 && I.wp_c == 0 && I.mq_c == 0;
+  }
+
+  // Returns true and the horizon (events with key < hz are run) when some
+  // chain-safe instance has an event before every other pending event;
+  // `per` is the list segment each participant gets.
+  AS_HD bool burst_select(const Head& h, Head& hz, bool safe[IPL], int& per) {
+    Head mine;
+    mine.code = -1;
+    mine.k = ~0ull;
+    mine.s = ~0u;
+    bool any_safe = false;
+#pragma unroll
+    for (int k = 0; k < IPL; k++) {
+      const Inst& I = st[k];
+      safe[k] = I.id >= 0 && chain_safe(I);
+      any_safe = any_safe || safe[k];
+      if (I.id >= 0 && I.busy && !safe[k]) offer(mine, I.ck, EV_ITER, I.iter_seq, 2 * I.id + 1);
+    }
+    if (!w.any(any_safe)) return false;
+    Head h2 = reduce_head(mine);
+    if (h.code >= 0 && (h2.code < 0 || h.k < h2.k || (h.k == h2.k && h.s < h2.s))) h2 = h;
+    uint64_t tmin = ~0ull;
+    int n_mine = 0;
+#pragma unroll
+    for (int k = 0; k < IPL; k++) {
+      const Inst& I = st[k];
+      const uint32_t k2 = ((uint32_t)EV_ITER << 28) | I.iter_seq;
+      safe[k] = safe[k] && (h2.code < 0 || I.ck < h2.k || (I.ck == h2.k && k2 < h2.s));
+      if (safe[k]) {
+        n_mine++;
+        if (I.ck < tmin) tmin = I.ck;
+      }
+    }
+    const uint32_t n_part = w.add_u32((uint32_t)n_mine);
+    if (n_part == 0) return false;
+    const uint32_t hi = w.min_u32((uint32_t)(tmin >> 32));
+    const uint32_t lo = w.min_u32((uint32_t)(tmin >> 32) == hi ? (uint32_t)tmin : ~0u);
+    per = (int)(BURST_POOL / n_part);
+    if (per > BURST_MAX) per = BURST_MAX;
+    // at most `per` events per instance: decode-only iterations last >= b1 + b0
+    const double t0 = okey_inv(((uint64_t)hi << 32) | lo);
+    const uint64_t cap = okey(t0 + (double)(per - 4) * (sc().b1 + sc().b0));
+    hz = h2;
+    if (hz.code < 0 || cap < hz.k) {
+      hz.k = cap;
+      hz.s = 0;
+      hz.code = 0;
+    }
+    bool run = false;
+#pragma unroll
+    for (int k = 0; k < IPL; k++) {
+      const uint32_t k2 = ((uint32_t)EV_ITER << 28) | st[k].iter_seq;
+      safe[k] = safe[k] && (st[k].ck < hz.k || (st[k].ck == hz.k && k2 < hz.s));
+      run = run || safe[k];
+    }
+    return w.any(run);
+  }
+
+  // Decode-only iteration chain of a chain-safe instance, from its pending
+  // completion up to the horizon: exactly execute_iteration + _kick for
+  // batches without prefill entries (instance.py:175-203, 229-288), with
+  // the scenario constants held in registers.  Writes each event's time key
+  // to `bk`; returns the events run and whether the last one pushed.
+  AS_HD int chain_run(Inst& I, uint64_t hz_k, int limit, uint64_t* bk, int& completed, int& last_pushed) {
+    const arrow_scenario_t& s = sc();
+    const double b1 = s.b1, b0 = s.b0;
+    const int kv_cap = s.kv_capacity;
+    const int dcap = imin(s.max_batch, s.chunk_budget);
+    double* ilog = (B->iterlog && have_om && om.iterlog_offset >= 0)
+                       ? B->iterlog + om.iterlog_offset + (int64_t)I.id * om.iterlog_stride
+                       : (double*)0;
+    const int64_t ilog_cap = ilog ? om.iterlog_stride : 0;
+    double* e = em(I.id);
+    int c = 0;
+    double t = I.busy_until;
+    uint64_t key = I.ck;
+    last_pushed = 0;
+    for (;;) {
+      const int cur = I.it - 1;
+      if (ilog) {
+        if (cur < ilog_cap)
+          ilog[cur] = t;
+        else if (u().overflow == ARROW_OVF_NONE)
+          u().overflow = ARROW_OVF_ITERLOG;
+      }
+      const int nd = I.pb_ndec;
+      I.kv_used += nd;
+      I.committed -= nd;
+      I.rtok += nd;
+      if (I.min_f == cur) {
+        int* rr = run_rid(I.id);
+        int* rf = run_f(I.id);
+        int m = 0x7fffffff, mc = 0;
+        int j = 0;
+        while (j < I.R) {
+          const int f = rf[j];
+          if (f == cur) {
+            const int rid = rr[j];
+            const int held = inl[rid] + outl[rid] - 1;
+            I.kv_used -= held;
+            I.rtok -= held;
+            p.last[rid] = t;
+            completed++;
+            I.R--;
+            rr[j] = rr[I.R];
+            rf[j] = rf[I.R];
+          } else {
+            if (f < m) {
+              m = f;
+              mc = 1;
+            } else if (f == m) {
+              mc++;
+            }
+            j++;
+          }
+        }
+        I.min_f = m;
+        I.min_f_cnt = mc;
+      }
+      // emission ring (lazy pruning, see interval())
+      if (I.em_c >= L.ecap) {
+        emit(I, t);
+      } else {
+        e[ring(I.em_h, I.em_c, L.ecap)] = t;
+        I.em_c++;
+      }
+      bk[c] = key;
+      c++;
+      // _kick: running decodes, then waiting decodes FCFS under the growth gate
+      int nd2 = I.R;
+      if (I.wd_c > 0 && nd2 < dcap) {
+        int kvf = kv_cap - I.kv_used - I.kv_reserved - I.committed;
+        const int* wd = wd_rid(I.id);
+        int ad = 0;
+        while (ad < I.wd_c && nd2 < dcap) {
+          const int g = outl[wd[ring(I.wd_h, ad, L.qcap)]] - 1;
+          if (g > kvf) break;
+          kvf -= g;
+          nd2++;
+          ad++;
+        }
+        if (ad > 0) {
+          const int ncur = I.it;
+          int* rr = run_rid(I.id);
+          int* rf = run_f(I.id);
+          int32_t* dit = (B->req_decode_iter && have_om && om.req_offset >= 0)
+                             ? B->req_decode_iter + om.req_offset
+                             : (int32_t*)0;
+          for (int j = 0; j < ad; j++) {
+            const int rid = wd[ring(I.wd_h, j, L.qcap)];
+            const int g = outl[rid] - 1;
+            const int f = ncur + g - 1;
+            if (I.R >= L.rcap) {
+              set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_RUNNING);
+              I.busy = 0;
+              return c;
+            }
+            rr[I.R] = rid;
+            rf[I.R] = f;
+            I.R++;
+            if (f < I.min_f) {
+              I.min_f = f;
+              I.min_f_cnt = 1;
+            } else if (f == I.min_f) {
+              I.min_f_cnt++;
+            }
+            I.committed += g;
+            I.wgrowth -= g;
+            if (dit) dit[rid] = ncur;
+          }
+          I.wd_h = ring(I.wd_h, ad, L.qcap);
+          I.wd_c -= ad;
+        }
+      } else if (I.R > dcap) {
+        set_status(ARROW_INTERNAL);
+      }
+      if (nd2 == 0) {             // nothing startable: the chain ends
+        I.busy = 0;
+        I.pb_ndec = 0;
+        return c;
+      }
+      I.it++;
+      I.pb_ndec = nd2;
+      t = t + (b1 * (double)nd2 + b0);
+      key = okey(t);
+      I.busy_until = t;
+      I.ck = key;
+      last_pushed = 1;
+      if (key >= hz_k) return c;
+      if (c >= limit) {           // the horizon bounds the count; never taken
+        set_status(ARROW_INTERNAL);
+        return c;
+      }
+      last_pushed = 0;
+    }
+  }
+
+  static AS_HD int lower_bound_u64(const uint64_t* a, int n, uint64_t x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (a[mid] < x)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    return lo;
+  }
+
+  AS_HD void run_burst(const bool safe[IPL], const Head& hz, int per) {
+    // segments: participant rank (slot-major, then lane) x per
+    int rank[IPL];
+    {
+      int base_rank = 0;
+#pragma unroll
+      for (int kk = 0; kk < IPL; kk++) {
+        const uint32_t m = w.ballot(safe[kk]);
+        rank[kk] = base_rank + popc32(m & ((1u << lane) - 1u));
+        base_rank += popc32(m);
+      }
+    }
+    int completed = 0, events = 0, pushes = 0;
+    int lastp[IPL];
+#pragma unroll
+    for (int k = 0; k < IPL; k++) {
+      lastp[k] = 0;
+      Inst& I = st[k];
+      if (!safe[k]) {
+        if (I.id >= 0) sm->bcount[I.id] = 0;
+        continue;
+      }
+      const int off = rank[k] * per;
+      sm->boff[I.id] = off;
+      sm->bseq[I.id] = I.iter_seq;
+      const int c = chain_run(I, hz.k, per, sm->blist + off, completed, lastp[k]);
+      sm->bcount[I.id] = c;
+      sm->blast[I.id] = lastp[k];
+      events += c;
+      pushes += c - 1 + lastp[k];
+    }
+    const uint32_t base = u().seq;
+    if (lane == 0) sm->btie = 0;
+    w.sync();
+    // The final pending push of each chain gets the global counter value it
+    // would have had: base + pushes (all chains) ordered before it.  Pushes
+    // inside the burst belong to events already executed, so their own
+    // numbers are never compared again.  Exact time ties with another
+    // chain's event fall back to a sequential merge.
+    int before[IPL];
+#pragma unroll
+    for (int k = 0; k < IPL; k++) before[k] = sm->bcount[st[k].id >= 0 ? st[k].id : 0] - 1;
+#pragma unroll
+    for (int kk = 0; kk < IPL; kk++) {
+      uint32_t m = w.ballot(safe[kk]);
+      while (m) {
+        const int j = ffs32(m);
+        m &= m - 1;
+        const int other = w.shfl(st[kk].id, j);
+        const uint64_t* lst = sm->blist + sm->boff[other];
+        const int n_o = sm->bcount[other];
+        const int last_o = sm->blast[other];
+#pragma unroll
+        for (int k = 0; k < IPL; k++) {
+          if (!safe[k] || !lastp[k] || st[k].id == other) continue;
+          const uint64_t x = sm->blist[sm->boff[st[k].id] + sm->bcount[st[k].id] - 1];
+          const int lb = lower_bound_u64(lst, n_o, x);
+          if (lb < n_o && lst[lb] == x) sm->btie = 1;
+          before[k] += lb - ((lb == n_o && !last_o) ? 1 : 0);
+        }
+      }
+    }
+    const uint32_t packed = w.add_u32((uint32_t)events | ((uint32_t)completed << 16));
+    const uint32_t total_push = w.add_u32((uint32_t)pushes);
+    w.sync();
+    const int tie = sm->btie;
+    if (!tie) {
+#pragma unroll
+      for (int k = 0; k < IPL; k++)
+        if (safe[k] && lastp[k]) st[k].iter_seq = base + (uint32_t)before[k];
+    } else {
+      // sequential merge of all chains in (time, seq) order; bseq[i] holds
+      // the sequence of chain i's current head event
+      lane0([&] {
+        const int N = sc().n_instances;
+        int* act = sm->list;
+        int na = 0;
+        for (int i = 0; i < N; i++) {
+          if (sm->bcount[i] > 0) {
+            act[na++] = i;
+            sm->bhead[i] = 0;
+          }
+        }
+        uint32_t seq = base;
+        while (na > 0) {
+          int best = 0;
+          uint64_t bk0 = sm->blist[sm->boff[act[0]] + sm->bhead[act[0]]];
+          for (int a2 = 1; a2 < na; a2++) {
+            const int i = act[a2];
+            const uint64_t kk = sm->blist[sm->boff[i] + sm->bhead[i]];
+            if (kk < bk0 || (kk == bk0 && sm->bseq[i] < sm->bseq[act[best]])) {
+              best = a2;
+              bk0 = kk;
+            }
+          }
+          const int i = act[best];
+          const int hd = sm->bhead[i];
+          const bool pushed = hd < sm->bcount[i] - 1 || sm->blast[i];
+          if (pushed) sm->bseq[i] = seq++;
+          sm->bhead[i] = hd + 1;
+          if (hd + 1 >= sm->bcount[i]) act[best] = act[--na];
+        }
+      });
+#pragma unroll
+      for (int k = 0; k < IPL; k++)
+        if (safe[k] && lastp[k]) st[k].iter_seq = sm->bseq[st[k].id];
+    }
+#pragma unroll
+    for (int k = 0; k < IPL; k++)
+      if (safe[k] && st[k].busy) classify(st[k]);
+    lane0([&] {
+      Uniform& U = u();
+      if (base + total_push >= SEQ_LIMIT) set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_SEQ);
+      U.seq = base + total_push;
+      U.esp = 0;
+      U.n_events += packed & 0xffffu;
+      U.n_iters += packed & 0xffffu;
+      U.completed += (int)(packed >> 16);
+      U.n_bursts++;
+    });
+  }
+
   AS_HD bool only_tick_pending() {
     bool active = false;
 #pragma unroll
@@ -1495,6 +1848,15 @@ struct Sim {
     Head h = full_scan();
     for (;;) {
       bool part[IPL];
+      Head hz;
+      int per = 0;
+      if (burst_select(h, hz, part, per)) {
+        run_burst(part, hz, per);
+        const int status = u().status;
+        w.sync();
+        if (status != ARROW_OK) return;
+        continue;
+      }
       if (round_select(h, part)) {
         run_round(part, h);
         const int status = u().status;
@@ -1728,8 +2090,9 @@ struct Sim {
       out->n_snapshots = U.n_snap;
       out->stall_time = U.status == ARROW_STALLED ? U.stall_time : NAN;
       out->decision_hash = U.hash;
-      out->reserved[0] = U.n_serial;   // serial (one-event) steps
-      out->reserved[1] = U.n_rounds;   // lane-parallel rounds
+      out->n_serial_steps = U.n_serial;
+      out->n_parallel_steps = U.n_rounds + U.n_bursts;
+      out->cycles = clock_now() - t_start;
       out->attainment = out->p90_ttft = out->p90_tpot = NAN;
       out->mean_ttft = out->mean_tpot = out->goodput = out->span = NAN;
     }
@@ -1746,7 +2109,18 @@ struct Sim {
     w.sync();
   }
 
+  int64_t t_start;
+
+  AS_HD static int64_t clock_now() {
+#ifdef __CUDA_ARCH__
+    return (int64_t)clock64();
+#else
+    return 0;
+#endif
+  }
+
   AS_HD void run(int s) {
+    t_start = clock_now();
     init_scenario(s);
     simulate();
     finish();
