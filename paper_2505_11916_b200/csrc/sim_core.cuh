@@ -1501,8 +1501,29 @@ struct Sim {
   // event lists (by time, ties by sequence) assigns the exact global push
   // sequence numbers the serial order would have produced.
 
+  // A queued migration can only start when KV is freed, i.e. at the
+  // completion of the iteration in which the earliest running decode
+  // finishes (min_f); with no decode waiting, the chain runs fixed batches
+  // of R decodes until then, so that completion time is exact arithmetic
+  // and bounds the burst.
+  // (Waiting decodes may be admitted without freed KV when they arrived
+  // after the last kick, which would change R and min_f: such chains only
+  // run when no migration can be pending.)
   AS_HD bool chain_safe(const Inst& I) const {
-    return I.busy && I.cq && I.rp_rid < 0 && I.wp_c == 0 && I.mq_c == 0;
+    return I.busy && I.cq && I.rp_rid < 0 && I.wp_c == 0 && !(I.mq_c > 0 && !I.mig_active && I.wd_c > 0);
+  }
+
+  AS_HD uint64_t chain_loud_bound(const Inst& I, uint64_t limit) const {
+    if (I.mq_c == 0 || I.mig_active) return ~0ull;
+    const int steps = I.min_f - (I.it - 1);   // >= 1: the pending event itself is quiet
+    const double dur = sc().b1 * (double)I.R + sc().b0;
+    double t = I.busy_until;
+    uint64_t k = I.ck;
+    for (int i = 0; i < steps && k < limit; i++) {
+      t = t + dur;
+      k = okey(t);
+    }
+    return k;
   }
 
   // Returns true and the horizon (events with key < hz are run) when some
@@ -1544,7 +1565,20 @@ struct Sim {
     if (per > BURST_MAX) per = BURST_MAX;
     // at most `per` events per instance: decode-only iterations last >= b1 + b0
     const double t0 = okey_inv(((uint64_t)hi << 32) | lo);
-    const uint64_t cap = okey(t0 + (double)(per - 4) * (sc().b1 + sc().b0));
+    uint64_t cap = okey(t0 + (double)(per - 4) * (sc().b1 + sc().b0));
+    {
+      uint64_t loud = ~0ull;
+#pragma unroll
+      for (int k = 0; k < IPL; k++)
+        if (safe[k]) {
+          const uint64_t b = chain_loud_bound(st[k], cap);
+          if (b < loud) loud = b;
+        }
+      const uint32_t lhi = w.min_u32((uint32_t)(loud >> 32));
+      const uint32_t llo = w.min_u32((uint32_t)(loud >> 32) == lhi ? (uint32_t)loud : ~0u);
+      const uint64_t lb = ((uint64_t)lhi << 32) | llo;
+      if (lb < cap) cap = lb;
+    }
     hz = h2;
     if (hz.code < 0 || cap < hz.k) {
       hz.k = cap;
@@ -1712,7 +1746,7 @@ struct Sim {
     return lo;
   }
 
-  AS_HD void run_burst(const bool safe[IPL], const Head& hz, int per) {
+  AS_HD void run_burst(const bool safe[IPL], const Head& hz, int per, Head& h) {
     // segments: participant rank (slot-major, then lane) x per
     int rank[IPL];
     {
@@ -1819,9 +1853,21 @@ struct Sim {
       for (int k = 0; k < IPL; k++)
         if (safe[k] && lastp[k]) st[k].iter_seq = sm->bseq[st[k].id];
     }
+    // a chain stopped at its migration bound leaves a loud pending event
+    Head loud;
+    loud.code = -1;
+    loud.k = ~0ull;
+    loud.s = ~0u;
 #pragma unroll
     for (int k = 0; k < IPL; k++)
-      if (safe[k] && st[k].busy) classify(st[k]);
+      if (safe[k] && st[k].busy) {
+        classify(st[k]);
+        if (!st[k].cq) offer(loud, st[k].ck, EV_ITER, st[k].iter_seq, 2 * st[k].id + 1);
+      }
+    if (w.any(loud.code >= 0)) {
+      Head nl = reduce_head(loud);
+      if (h.code < 0 || nl.k < h.k || (nl.k == h.k && nl.s < h.s)) h = nl;
+    }
     lane0([&] {
       Uniform& U = u();
       if (base + total_push >= SEQ_LIMIT) set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_SEQ);
@@ -1851,7 +1897,7 @@ struct Sim {
       Head hz;
       int per = 0;
       if (burst_select(h, hz, part, per)) {
-        run_burst(part, hz, per);
+        run_burst(part, hz, per, h);
         const int status = u().status;
         w.sync();
         if (status != ARROW_OK) return;

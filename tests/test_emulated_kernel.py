@@ -48,3 +48,26 @@ def test_emulated_kernel_batch_of_scenarios():
         hb = H.run_emu(cb, width=8)
         for s, (m, a) in enumerate(group):
             H.check_vs_golden(m, a, hb, s)
+
+
+@pytest.mark.parametrize("index", [9, 27, 41, 52, 84])
+def test_emulated_kernel_matches_oracle_on_c2_points(index):
+    """C2 sweep points under heavy KV pressure (queued migrations, waiting
+    decodes, flips) — where chain bursts must stop before loud events —
+    against the CPU oracle: every summary field and per-request time."""
+    from paper_2505_11916_b200 import workloads as W
+    from paper_2505_11916_b200._buffers import OutputSpec
+    from paper_2505_11916_b200._compile import compile_batch
+
+    cb = compile_batch([W.c2()[index]], 500_000)
+    spec = OutputSpec(requests=True, decisions=True)
+    got = H.run_emu(cb, spec, width=8)
+    exp = H.run_oracle(cb, spec)
+    g, e = got.summaries[0], exp.summaries[0]
+    for f in ("status", "n_completed", "n_ok", "n_flips", "n_events", "n_iterations", "n_decisions", "decision_hash"):
+        assert int(g[f]) == int(e[f]), f
+    H.assert_same_f64(got.req_first, exp.req_first, "first")
+    H.assert_same_f64([g["stall_time"]], [e["stall_time"]], "stall time")
+    if int(e["status"]) == 0:       # a stalled run raises; its partial records are never observed
+        H.assert_same_f64(got.req_last, exp.req_last, "last")
+        H.assert_same_decisions(got.decisions_of(0), exp.decisions_of(0))

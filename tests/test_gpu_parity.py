@@ -92,7 +92,10 @@ def test_random_sweep_matches_oracle(evaluator, seed):
         for f in ("stall_time", "attainment", "p90_ttft", "p90_tpot", "mean_ttft", "mean_tpot", "goodput", "span"):
             H.assert_same_f64([g[f]], [e[f]], f"scenario {s} {f}")
     H.assert_same_f64(got.req_first, exp.req_first, "first")
-    H.assert_same_f64(got.req_last, exp.req_last, "last")
+    for s in range(cb.n):
+        if int(exp.summaries[s]["status"]) == _abi.OK:   # stalled runs raise; partial records unobserved
+            sl = got.req_slice(s)
+            H.assert_same_f64(got.req_last[sl], exp.req_last[sl], f"scenario {s} last")
     np.testing.assert_array_equal(got.req_prefill, exp.req_prefill)
     np.testing.assert_array_equal(got.req_decode, exp.req_decode)
     assert (got.summaries["status"] == _abi.OK).sum() > 0
