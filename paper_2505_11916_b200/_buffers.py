@@ -105,7 +105,7 @@ class HostBuffers:
         self.order = None if order is None else np.ascontiguousarray(order, dtype=np.int32)
         self.summaries = np.zeros(cb.n, dtype=_abi.SUMMARY_DTYPE)
         self.outmap = lay.outmap
-        one = lambda n, dt: np.zeros(max(n, 1), dtype=dt) if n else None  # noqa: E731
+        one = lambda n, dt: np.zeros(max(n, 1), dtype=dt)  # noqa: E731
         self.req_first = one(lay.n_req, np.float64) if spec.requests else None
         self.req_last = one(lay.n_req, np.float64) if spec.requests else None
         self.req_prefill = one(lay.n_req, np.int32) if spec.requests else None
