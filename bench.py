@@ -48,7 +48,12 @@ def workload(name: str, rank: int):
     if name == "c5":
         total = 4 * 32 * 3 * 4 * 4 * 4 * 4
         ids = np.arange(rank, total, int(os.environ.get("WORLD_SIZE", "1")))
-        return W.c5(ids), "C5 mixed-radix sweep shard (98304 scenarios total)"
+        sample = int(os.environ.get("ARROW_C5_SAMPLE", "0"))
+        desc = "C5 mixed-radix sweep shard (98304 scenarios total, static interleave)"
+        if sample:
+            ids = np.sort(np.random.default_rng(5).choice(ids, size=min(sample, len(ids)), replace=False))
+            desc += f", seeded random sample of {len(ids)} scenarios per rank"
+        return W.c5(ids), desc
     if name == "c1":
         return W.c1(), "C1 single Arrow simulation, 4 instances, 1000 requests @4 req/s"
     raise SystemExit(f"unknown workload {name}")
@@ -190,7 +195,7 @@ def run_ours(args, rank: int, world: int) -> None:
 
     from paper_2505_11916_b200._backend import CudaEvaluator
     from paper_2505_11916_b200._buffers import OutputSpec
-    from paper_2505_11916_b200._compile import compile_batch
+    from paper_2505_11916_b200._compile import compile_batch, dispatch_order
     from paper_2505_11916_b200 import engine, _abi
     from paper_2505_11916_b200.sweep import evaluate_scenarios
 
@@ -206,7 +211,7 @@ def run_ours(args, rank: int, world: int) -> None:
     ev = CudaEvaluator(dev)
     cb = compile_batch(scenarios, engine.STALL_EVENT_LIMIT)
     spec = OutputSpec()
-    db = ev.prepare(cb, spec)
+    db = ev.prepare(cb, spec, dispatch_order(cb))
     stream = torch.cuda.current_stream(dev)
     n_req = int(cb.scenarios["n_requests"].sum())
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)     # > 126 MB L2

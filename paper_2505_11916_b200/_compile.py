@@ -258,3 +258,22 @@ def compile_batch(scenarios: list[Scenario], stall_limit: int, validate: bool = 
         fifo_capacity=max_n,
     )
     return CompiledBatch(arrival, inp, outp, recs, table, tix, sizes)
+
+
+def dispatch_order(cb: CompiledBatch) -> np.ndarray:
+    """Longest-first dispatch order for the persistent kernel's work queue.
+
+    A scenario's device time is dominated by its iteration count, roughly
+    its total output tokens divided by the average decode batch, which
+    shrinks as the per-instance arrival rate falls.  The estimate only
+    orders work; results do not depend on it."""
+    est = np.zeros(cb.n)
+    for k in range(cb.n):
+        e = cb.table.entries[cb.trace_index[k]]
+        n = len(e.arrival)
+        if n < 2:
+            continue
+        span = (float(e.arrival[-1]) - float(e.arrival[0])) * float(cb.scenarios["arrival_scale"][k])
+        per_inst = (n - 1) / max(span, 1e-9) / max(int(cb.scenarios["n_instances"][k]), 1)
+        est[k] = float(e.output_len.sum()) / (1.0 + per_inst)
+    return np.argsort(-est, kind="stable").astype(np.int32)

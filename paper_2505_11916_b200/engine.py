@@ -13,7 +13,7 @@ from dataclasses import dataclass, field, replace
 
 from . import _results
 from ._buffers import OutputSpec
-from ._compile import Scenario, compile_batch
+from ._compile import Scenario, compile_batch, dispatch_order
 from .config import (  # noqa: F401  (re-exported like the reference module)
     CONFIG_KEYS as _CONFIG_KEYS,
     DEFAULTS as _DEFAULTS,
@@ -57,6 +57,8 @@ def execute(scenarios: list[Scenario], spec: OutputSpec, evaluator=None, order=N
 
     ev = evaluator or default_evaluator()
     cb = compile_batch(scenarios, STALL_EVENT_LIMIT)
+    if order is None and cb.n > 1:
+        order = dispatch_order(cb)
     while True:
         hb = ev.execute(cb, spec, order)
         ovf = hb.summaries["overflow"]
