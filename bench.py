@@ -118,6 +118,25 @@ def peaks() -> dict:
     return {"hbm_gbs": 6650.0, "source": "fallback"}
 
 
+def ncu_traffic(workload: str):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
+    from the committed `ncu --set full` capture of this bench's kernel
+    (profiles/<workload>_kernel_ncu_raw.csv), or None."""
+    import csv
+
+    path = ROOT / "profiles" / f"{workload}_kernel_ncu_raw.csv"
+    if not path.exists():
+        return None
+    rows = list(csv.reader(path.open()))
+    head, units, vals = rows[0], rows[1], rows[2]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    total = 0.0
+    for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        i = head.index(name)
+        total += float(vals[i]) * scale.get(units[i], 1)
+    return total
+
+
 def cpu_port_baseline(scenarios, budget_s: float, threads: int) -> dict:
     """The C port of the reference (oracle/) on a bounded, evenly spaced
     sample of the step's scenarios, all host threads."""
@@ -290,7 +309,8 @@ def run_ours(args, rank: int, world: int) -> None:
         "peak": pk["hbm_gbs"],
         "unit": "GB/s",
         "frac": achieved / pk["hbm_gbs"],
-        "traffic": None,
+        "traffic": ncu_traffic(args.workload),
+        "traffic_source": f"profiles/{args.workload}_kernel_ncu_raw.csv (ncu --set full, one launch)",
         "peak_source": pk["source"],
         "note": "latency-bound serial event chains; algorithmic bytes = 40 B/request + 256 B/scenario",
     }
