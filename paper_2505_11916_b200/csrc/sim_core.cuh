@@ -140,6 +140,7 @@ struct Uniform {
   int64_t n_events, n_iters, n_ticks, n_snap, n_dec;
   int64_t rr_p, rr_d;
   int64_t n_rounds, n_serial, n_bursts;
+  int64_t cyc_serial, cyc_round, cyc_burst;   // profiling: SM cycles by step kind
   uint64_t hash;
   uint32_t seq, tick_seq;
   int a;
@@ -192,7 +193,10 @@ struct Inst {
   int parked;
   int min_f_cnt;                // running decodes finishing at min_f
   int pb_pc, pb_emit;           // pending iteration pushes a PREFILL_COMPLETE / emits a token
-  int pb_rel;                   // pending iteration releases a single-token request's KV
+  int pb_rel;                   // KV released by single-token requests completing in the pending iteration
+  int pb_rp_left;               // the running partial prompt survives the pending iteration
+  int held_min;                 // KV held by the running decodes finishing at min_f
+  int mq_need;                  // KV need of the migration queue head (valid when mq_c > 0)
   int cq;                       // cached: pending iteration is quiet
   uint64_t ck;                  // cached: order key of busy_until
   double dly;                   // predicted_prefill_delay at the current event
@@ -457,6 +461,10 @@ struct Sim {
     if (kvf - I.wgrowth < need) return false;
     I.mq_h = I.mq_h + 1 == L.qcap ? 0 : I.mq_h + 1;
     I.mq_c--;
+    if (I.mq_c > 0) {
+      const int nr = mq_rid(I.id)[I.mq_h];
+      I.mq_need = inl[nr] + (outl[nr] - 1);
+    }
     I.kv_reserved += inl[rid];
     I.mig_active = 1;
     I.mig_rid = rid;
@@ -509,7 +517,7 @@ struct Sim {
         planned = true;
         done_pf = 1;
         pc = outl[rid] > 1;
-        rel = outl[rid] == 1;
+        rel = outl[rid] == 1 ? len : 0;
       }
     }
     if (!planned) {
@@ -531,7 +539,7 @@ struct Sim {
             if (c == rem) {
               done_pf++;
               pc |= outl[I.rp_rid] > 1;
-              rel |= outl[I.rp_rid] == 1;
+              rel += outl[I.rp_rid] == 1 ? inl[I.rp_rid] : 0;
             }
           }
         }
@@ -548,7 +556,7 @@ struct Sim {
         if (last_comp) {
           done_pf++;
           pc |= outl[rid] > 1;
-          rel |= outl[rid] == 1;
+          rel += outl[rid] == 1 ? rem : 0;
         }
         left -= c;
         kvf -= c;
@@ -574,11 +582,14 @@ struct Sim {
         rr[I.R] = rid;
         rf[I.R] = f;
         I.R++;
+        const int held = inl[rid] + g;
         if (f < I.min_f) {
           I.min_f = f;
           I.min_f_cnt = 1;
+          I.held_min = held;
         } else if (f == I.min_f) {
           I.min_f_cnt++;
+          I.held_min += held;
         }
         I.committed += g;
         I.wgrowth -= g;
@@ -597,6 +608,7 @@ struct Sim {
     I.pb_ded = ded;
     I.pb_pc = pc;
     I.pb_rel = rel;
+    I.pb_rp_left = I.rp_rid >= 0 && !(rp_chunk > 0 && rp_chunk == inl[I.rp_rid] - I.rp_done);
     I.pb_emit = (nd + done_pf) > 0;
     double dur = ded ? quad(s.true_a2, s.true_a1, s.true_a0, last_chunk) : s.b1 * (double)total + s.b0;
     I.busy_until = now + dur;
@@ -649,7 +661,7 @@ struct Sim {
       if (I.min_f == cur) {
         int* rr = run_rid(I.id);
         int* rf = run_f(I.id);
-        int m = 0x7fffffff, mc = 0;
+        int m = 0x7fffffff, mc = 0, mh = 0;
         int j = 0;
         while (j < I.R) {
           int f = rf[j];
@@ -664,17 +676,21 @@ struct Sim {
             rr[j] = rr[I.R];
             rf[j] = rf[I.R];
           } else {
+            const int hh = inl[rr[j]] + outl[rr[j]] - 1;
             if (f < m) {
               m = f;
               mc = 1;
+              mh = hh;
             } else if (f == m) {
               mc++;
+              mh += hh;
             }
             j++;
           }
         }
         I.min_f = m;
         I.min_f_cnt = mc;
+        I.held_min = mh;
       }
     }
     if (I.pb_rp_chunk > 0) {
@@ -1085,6 +1101,7 @@ struct Sim {
           return;
         }
         mq_rid(I.id)[ring(I.mq_h, I.mq_c, L.qcap)] = rid;
+        if (I.mq_c == 0) I.mq_need = inl[rid] + (outl[rid] - 1);
         I.mq_c++;
         if (start_mig(I, now)) I.mig_seq = next_seq();
         if (kick(I, now)) I.iter_seq = next_seq();
@@ -1305,16 +1322,31 @@ struct Sim {
   // the round's pushes get their exact global sequence numbers by ranking the
   // round's events by (time, seq).  Returns:
 
-  // A queued migration can only start at this completion if the iteration
-  // frees KV: X = kv_free - waiting growth never increases between
-  // handlers without a start_mig attempt (instance.py:140 gate failed at a
-  // state >= the current one), and executing an iteration changes X only by
-  // finished decodes and released single-token prompts.
+  // Exact test of whether this completion has effects beyond its own
+  // instance (engine.py:205-223): a PREFILL_COMPLETE push, a migration start
+  // or a drained-pool move; or emits no token (stall counter).
+  //  * migration: advance_migrations' gate (instance.py:140) compares
+  //    X = kv_free - waiting growth with the queue head's need; executing
+  //    the iteration raises X exactly by the KV of the decodes finishing at
+  //    it and of released single-token prompts, and between handlers X
+  //    never rises without a start_mig attempt, so the gate passes iff
+  //    X_now + freed >= need.
+  //  * drain (engine.py:183-192): the prefill / decode work left after the
+  //    iteration is known from the pending batch.
   AS_HD bool quiet(const Inst& I) const {
+    if (!I.busy || !I.pb_emit || I.pb_pc) return false;
+    const int cur = I.it - 1;
+    const int fin = I.min_f == cur ? I.min_f_cnt : 0;
+    if (I.mq_c > 0 && !I.mig_active && (fin > 0 || I.pb_rel > 0)) {
+      const int x = sc().kv_capacity - I.kv_used - I.kv_reserved - I.committed - I.wgrowth;
+      const int freed = (fin > 0 ? I.held_min : 0) + I.pb_rel;
+      if (x + freed >= I.mq_need) return false;
+    }
     const int pk = pool_of(I.id);
-    const bool frees = I.min_f == I.it - 1 || I.pb_rel;
-    return I.busy && I.pb_emit && !I.pb_pc && (pk == P_PREFILL || pk == P_DECODE) &&
-           !(I.mq_c > 0 && !I.mig_active && frees);
+    if (pk == P_P2D)
+      return I.wp_c > I.pb_k || I.pb_rp_left || (I.pb_k > 0 && !I.pb_last_comp);
+    if (pk == P_D2P) return I.mig_active || I.mq_c > 0 || I.wd_c > 0 || I.R - fin > 0;
+    return true;
   }
 
   // Lower bound on the duration of the iteration this instance starts when
@@ -1510,7 +1542,9 @@ struct Sim {
   // after the last kick, which would change R and min_f: such chains only
   // run when no migration can be pending.)
   AS_HD bool chain_safe(const Inst& I) const {
-    return I.busy && I.cq && I.rp_rid < 0 && I.wp_c == 0 && !(I.mq_c > 0 && !I.mig_active && I.wd_c > 0);
+    const int pk = pool_of(I.id);
+    return I.busy && I.cq && I.rp_rid < 0 && I.wp_c == 0 && (pk == P_PREFILL || pk == P_DECODE) &&
+           !(I.mq_c > 0 && !I.mig_active && I.wd_c > 0);
   }
 
   AS_HD uint64_t chain_loud_bound(const Inst& I, uint64_t limit) const {
@@ -1629,7 +1663,7 @@ struct Sim {
       if (I.min_f == cur) {
         int* rr = run_rid(I.id);
         int* rf = run_f(I.id);
-        int m = 0x7fffffff, mc = 0;
+        int m = 0x7fffffff, mc = 0, mh = 0;
         int j = 0;
         while (j < I.R) {
           const int f = rf[j];
@@ -1644,17 +1678,21 @@ struct Sim {
             rr[j] = rr[I.R];
             rf[j] = rf[I.R];
           } else {
+            const int hh = inl[rr[j]] + outl[rr[j]] - 1;
             if (f < m) {
               m = f;
               mc = 1;
+              mh = hh;
             } else if (f == m) {
               mc++;
+              mh += hh;
             }
             j++;
           }
         }
         I.min_f = m;
         I.min_f_cnt = mc;
+        I.held_min = mh;
       }
       // emission ring (lazy pruning, see interval())
       if (I.em_c >= L.ecap) {
@@ -1697,11 +1735,14 @@ struct Sim {
             rr[I.R] = rid;
             rf[I.R] = f;
             I.R++;
+            const int held = inl[rid] + g;
             if (f < I.min_f) {
               I.min_f = f;
               I.min_f_cnt = 1;
+              I.held_min = held;
             } else if (f == I.min_f) {
               I.min_f_cnt++;
+              I.held_min += held;
             }
             I.committed += g;
             I.wgrowth -= g;
@@ -1896,8 +1937,10 @@ struct Sim {
       bool part[IPL];
       Head hz;
       int per = 0;
+      const int64_t c0 = clock_now();
       if (burst_select(h, hz, part, per)) {
         run_burst(part, hz, per, h);
+        if (lane == 0) u().cyc_burst += clock_now() - c0;
         const int status = u().status;
         w.sync();
         if (status != ARROW_OK) return;
@@ -1905,6 +1948,7 @@ struct Sim {
       }
       if (round_select(h, part)) {
         run_round(part, h);
+        if (lane == 0) u().cyc_round += clock_now() - c0;
         const int status = u().status;
         w.sync();
         if (status != ARROW_OK) return;
@@ -1967,6 +2011,8 @@ struct Sim {
           owner(id, [&](Inst& I) {
             int completed = 0;
             bool pushed = false;
+            ATRACE("loud inst %d pc %d emit %d pool %d mq %d ma %d frees %d\n", I.id, I.pb_pc, I.pb_emit, pool_of(I.id),
+                   I.mq_c, I.mig_active, (int)(I.min_f == I.it - 1 || I.pb_rel));
             u().n_iters++;
             u().tmp_i[0] = iteration_complete<true>(I, now, completed, pushed);
             u().completed += completed;
@@ -1990,6 +2036,7 @@ struct Sim {
         return;
       }
       h = full_scan();
+      if (lane == 0) u().cyc_serial += clock_now() - c0;
     }
     // end-of-run checks, engine.py:286-290
     const int completed = u().completed;
@@ -2139,6 +2186,10 @@ struct Sim {
       out->n_serial_steps = U.n_serial;
       out->n_parallel_steps = U.n_rounds + U.n_bursts;
       out->cycles = clock_now() - t_start;
+      {  // profiling: per-mille of loop cycles in serial steps (high word) and rounds (low word)
+        const int64_t tot = U.cyc_serial + U.cyc_round + U.cyc_burst + 1;
+        out->reserved = ((U.cyc_serial * 1000 / tot) << 32) | (U.cyc_round * 1000 / tot);
+      }
       out->attainment = out->p90_ttft = out->p90_tpot = NAN;
       out->mean_ttft = out->mean_tpot = out->goodput = out->span = NAN;
     }

@@ -99,3 +99,38 @@ def test_random_sweep_matches_oracle(evaluator, seed):
     np.testing.assert_array_equal(got.req_prefill, exp.req_prefill)
     np.testing.assert_array_equal(got.req_decode, exp.req_decode)
     assert (got.summaries["status"] == _abi.OK).sum() > 0
+
+
+def test_large_clusters_two_instances_per_lane(evaluator):
+    """N > 32 puts two instances on each lane (register slots 0 and 1):
+    C4-style clusters of 33-64 instances against the CPU oracle."""
+    import sys
+
+    sys.path.insert(0, str(H.ROOT / "oracle"))
+    import scenarios as S
+    from paper_2505_11916_b200.config import config_from_values
+    from paper_2505_11916_b200.core import TraceRequest
+
+    trace = S.synthetic(TraceRequest, 600.0, 4.0, np.log(420.0), 0.55, np.log(130.0), 0.5,
+                        ((100.0, 60.0, 5.0), (300.0, 90.0, 4.0)), 3500, 900, 3)[:2000]
+    scs = []
+    for k, (N, strat, td, rate_per) in enumerate([(33, "slo-aware", 0.5, 1.25), (48, "slo-aware", 0.25, 2.5),
+                                                   (64, "slo-aware", 1.0, 2.5), (40, "minimal-load", 0.5, 2.0),
+                                                   (64, "round-robin", 0.5, 1.0), (64, "slo-aware", 0.75, 4.0)]):
+        v = S.cfg(instances=N, init_prefill=N // 2, init_decode=N - N // 2, strategy=strat, theta_d=td,
+                  kv_capacity_tokens=6000)
+        scs.append(Scenario(trace, config_from_values(v), S.rate_scale(trace, rate_per * N), k))
+    cb = compile_batch(scs, 500_000)
+    assert cb.sizes["max_instances"] == 64
+    spec = OutputSpec(requests=True, decisions=True)
+    got = evaluator.execute(cb, spec)
+    exp = H.run_oracle(cb, spec, threads=0)
+    for s in range(cb.n):
+        g, e = got.summaries[s], exp.summaries[s]
+        for f in ("status", "n_completed", "n_ok", "n_flips", "n_events", "n_iterations", "n_decisions",
+                  "decision_hash"):
+            assert int(g[f]) == int(e[f]), (s, f, g[f], e[f])
+        if int(e["status"]) == _abi.OK:
+            H.assert_same_decisions(got.decisions_of(s), exp.decisions_of(s))
+            sl = got.req_slice(s)
+            H.assert_same_f64(got.req_last[sl], exp.req_last[sl], f"scenario {s} last")
