@@ -197,6 +197,7 @@ struct Inst {
   int pb_rp_left;               // the running partial prompt survives the pending iteration
   int held_min;                 // KV held by the running decodes finishing at min_f
   int mq_need;                  // KV need of the migration queue head (valid when mq_c > 0)
+  double em_first, em_last;     // oldest / newest time in the emission ring (valid when em_c > 0)
   int cq;                       // cached: pending iteration is quiet
   uint64_t ck;                  // cached: order key of busy_until
   double dly;                   // predicted_prefill_delay at the current event
@@ -417,23 +418,38 @@ struct Sim {
   // is exact because query times never decrease.
   AS_HD bool interval(Inst& I, double now, double* out) {
     const double lo = now - sc().window;
-    const double* e = em(I.id);
-    if (I.em_c > 0 && e[I.em_h] < lo) {
-      int a = 0, b = I.em_c;          // first offset with t >= lo lies in (a, b]
+    if (I.em_c > 0 && I.em_first < lo) {
+      // gallop from the head, then binary search: the first offset with t >= lo
+      const double* e = em(I.id);
+      int a = 0, b = 0, step = 1;
+      double vb = 0.0;
+      for (;;) {
+        b = a + step;
+        if (b >= I.em_c) {
+          b = I.em_c;
+          break;
+        }
+        vb = e[ring(I.em_h, b, L.ecap)];
+        if (vb >= lo) break;
+        a = b;
+        step <<= 1;
+      }
       while (b - a > 1) {
-        int mid = (a + b) >> 1;
-        if (e[ring(I.em_h, mid, L.ecap)] < lo)
+        const int mid = (a + b) >> 1;
+        const double vm = e[ring(I.em_h, mid, L.ecap)];
+        if (vm < lo) {
           a = mid;
-        else
+        } else {
           b = mid;
+          vb = vm;
+        }
       }
       I.em_h = ring(I.em_h, b, L.ecap);
       I.em_c -= b;
+      if (I.em_c > 0) I.em_first = vb;
     }
     if (I.em_c < 2) return false;
-    const double first = e[I.em_h];
-    const double last = e[ring(I.em_h, I.em_c - 1, L.ecap)];
-    *out = (last - first) / (double)(I.em_c - 1);
+    *out = (I.em_last - I.em_first) / (double)(I.em_c - 1);
     return true;
   }
 
@@ -448,6 +464,8 @@ struct Sim {
       }
     }
     e[ring(I.em_h, I.em_c, L.ecap)] = now;
+    if (I.em_c == 0) I.em_first = now;
+    I.em_last = now;
     I.em_c++;
   }
 
@@ -1699,6 +1717,8 @@ struct Sim {
         emit(I, t);
       } else {
         e[ring(I.em_h, I.em_c, L.ecap)] = t;
+        if (I.em_c == 0) I.em_first = t;
+        I.em_last = t;
         I.em_c++;
       }
       bk[c] = key;
