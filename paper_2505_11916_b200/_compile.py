@@ -151,7 +151,9 @@ class TraceTable:
             z = np.zeros(1, dtype=np.float64)
             return z, np.ones(1, dtype=np.int32), np.ones(1, dtype=np.int32)
         return (
-            np.concatenate([e.arrival for e in self.entries]),
+            # + 0.0 canonicalises -0.0 (Python compares it equal to 0.0; the
+            # device orders event times by bit pattern)
+            np.concatenate([e.arrival for e in self.entries]) + 0.0,
             np.concatenate([e.input_len for e in self.entries]).astype(np.int32),
             np.concatenate([e.output_len for e in self.entries]).astype(np.int32),
         )

@@ -216,6 +216,14 @@ AS_HD uint64_t okey(double x) {
   return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
 
+// Order key of an event time: event times are never -0.0 (arrivals are
+// canonicalised on the host; every other time is t + positive duration), so
+// no canonicalising add is needed.
+AS_HD uint64_t tkey(double t) {
+  const uint64_t u = dbits(t);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
 AS_HD double okey_inv(uint64_t k) {
   uint64_t u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
   double x;
@@ -375,8 +383,8 @@ struct Sim {
   AS_HD double* em(int id) { return p.em + (int64_t)id * L.ecap; }
 
   AS_HD int ring(int h, int j, int64_t cap) const {
-    int64_t x = (int64_t)h + j;
-    return (int)(x >= cap ? x - cap : x);
+    const int x = h + j;                  // h, j < cap <= 2^30
+    return x >= (int)cap ? x - (int)cap : x;
   }
 
   // -------------------------------------------- instance-local (owner) --
@@ -1394,7 +1402,7 @@ struct Sim {
   }
 
   AS_HD void classify(Inst& I) const {
-    I.ck = okey(I.busy_until);
+    I.ck = tkey(I.busy_until);
     I.cq = quiet(I) ? 1 : 0;
   }
 
@@ -1428,14 +1436,14 @@ struct Sim {
         classify(I);
         if (!I.cq) offer(mine, I.ck, EV_ITER, I.iter_seq, 2 * I.id + 1);
       }
-      if (I.mig_active) offer(mine, okey(I.mig_finish), EV_MIG, I.mig_seq, 2 * I.id);
+      if (I.mig_active) offer(mine, tkey(I.mig_finish), EV_MIG, I.mig_seq, 2 * I.id);
     }
     if (lane == 0) {
       const Uniform& U = sm->u;
-      if (U.a < sc().n_requests) offer(mine, okey(U.next_arrival), EV_ARRIVAL, (uint32_t)U.a, 1000 + EV_ARRIVAL);
+      if (U.a < sc().n_requests) offer(mine, tkey(U.next_arrival), EV_ARRIVAL, (uint32_t)U.a, 1000 + EV_ARRIVAL);
       if (U.fifo_count > 0)
-        offer(mine, okey(p.fifo_time[U.fifo_head]), EV_PREFILL, p.fifo_seq[U.fifo_head], 1000 + EV_PREFILL);
-      if (U.tick_active) offer(mine, okey(U.tick_time), EV_TICK, U.tick_seq, 1000 + EV_TICK);
+        offer(mine, tkey(p.fifo_time[U.fifo_head]), EV_PREFILL, p.fifo_seq[U.fifo_head], 1000 + EV_PREFILL);
+      if (U.tick_active) offer(mine, tkey(U.tick_time), EV_TICK, U.tick_seq, 1000 + EV_TICK);
     }
     return reduce_head(mine);
   }
@@ -1453,7 +1461,7 @@ struct Sim {
       cand[k] = I.id >= 0 && I.busy && I.cq && (h.code < 0 || I.ck < h.k || (I.ck == h.k && k2 < h.s));
       if (cand[k]) {
         any_cand = true;
-        const uint64_t x = okey(I.busy_until + next_duration_bound(I));
+        const uint64_t x = tkey(I.busy_until + next_duration_bound(I));
         if (x < lim) lim = x;
       }
     }
@@ -1480,7 +1488,7 @@ struct Sim {
       key2[k] = 0;
       if (!part[k]) continue;
       Inst& I = st[k];
-      key1[k] = okey(I.busy_until);
+      key1[k] = tkey(I.busy_until);
       key2[k] = I.iter_seq;
       n_part++;
       iteration_complete<false>(I, I.busy_until, completed, pushed[k]);
@@ -1569,13 +1577,10 @@ struct Sim {
     if (I.mq_c == 0 || I.mig_active) return ~0ull;
     const int steps = I.min_f - (I.it - 1);   // >= 1: the pending event itself is quiet
     const double dur = sc().b1 * (double)I.R + sc().b0;
+    const double tlim = okey_inv(limit);
     double t = I.busy_until;
-    uint64_t k = I.ck;
-    for (int i = 0; i < steps && k < limit; i++) {
-      t = t + dur;
-      k = okey(t);
-    }
-    return k;
+    for (int i = 0; i < steps && t < tlim; i++) t = t + dur;
+    return tkey(t);
   }
 
   // Returns true and the horizon (events with key < hz are run) when some
@@ -1617,7 +1622,7 @@ struct Sim {
     if (per > BURST_MAX) per = BURST_MAX;
     // at most `per` events per instance: decode-only iterations last >= b1 + b0
     const double t0 = okey_inv(((uint64_t)hi << 32) | lo);
-    uint64_t cap = okey(t0 + (double)(per - 4) * (sc().b1 + sc().b0));
+    uint64_t cap = tkey(t0 + (double)(per - 4) * (sc().b1 + sc().b0));
     {
       uint64_t loud = ~0ull;
 #pragma unroll
@@ -1782,7 +1787,7 @@ struct Sim {
       I.it++;
       I.pb_ndec = nd2;
       t = t + (b1 * (double)nd2 + b0);
-      key = okey(t);
+      key = tkey(t);
       I.busy_until = t;
       I.ck = key;
       last_pushed = 1;
