@@ -1,7 +1,7 @@
 # Builds (all in-tree; .so files are git-ignored but travel to the GPU box)
 #   make lib      CUDA evaluator   paper_2505_11916_b200/lib/libarrow_sim.so  (sm_100a)
 #   make oracle   CPU oracle       oracle/build/libpdsim_oracle.so            (test infra)
-#   make emu      host emulator    build/libarrow_emu.so                      (test infra)
+#   make emu      host emulators   build/libarrow_emu.so, build/libnpgen_host.so (test infra)
 NVCC ?= /usr/local/cuda/bin/nvcc
 CXX_HOST ?= g++
 ARCH := -gencode arch=compute_100a,code=sm_100a
@@ -9,7 +9,9 @@ PKG := paper_2505_11916_b200
 CSRC := $(PKG)/csrc
 LIBDIR := $(PKG)/lib
 LIB := $(LIBDIR)/libarrow_sim.so
-HDRS := include/arrow_sim.h $(CSRC)/sim_core.cuh $(CSRC)/warp.cuh
+HDRS := include/arrow_sim.h include/arrow_traces.h $(CSRC)/sim_core.cuh $(CSRC)/warp.cuh \
+	$(CSRC)/npgen.cuh $(CSRC)/npgen_tables.h
+SRCS := $(CSRC)/arrow_sim.cu $(CSRC)/traces.cu
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -fmad=false -prec-div=true -Xptxas -v \
 	-Xcompiler -fPIC,-ffp-contract=off -Iinclude -I$(CSRC) --shared
 
@@ -17,19 +19,24 @@ all: lib oracle emu
 
 lib: $(LIB)
 
-$(LIB): $(CSRC)/arrow_sim.cu $(HDRS)
+$(LIB): $(SRCS) $(HDRS)
 	@mkdir -p $(LIBDIR)
-	$(NVCC) $(NVFLAGS) -o $@ $(CSRC)/arrow_sim.cu 2> $(LIBDIR)/ptxas.log || (cat $(LIBDIR)/ptxas.log; exit 1)
+	$(NVCC) $(NVFLAGS) -o $@ $(SRCS) 2> $(LIBDIR)/ptxas.log || (cat $(LIBDIR)/ptxas.log; exit 1)
 
 oracle:
 	$(MAKE) -s -C oracle
 
-emu: build/libarrow_emu.so
+emu: build/libarrow_emu.so build/libnpgen_host.so
 
 build/libarrow_emu.so: $(CSRC)/emu/emu.cpp $(HDRS)
 	@mkdir -p build
 	$(CXX_HOST) -std=c++20 -O2 -g -fPIC -shared -ffp-contract=off -fno-fast-math -pthread \
 		-Wall -Wno-unknown-pragmas -DARROW_EMU_TRACE -Iinclude -o $@ $(CSRC)/emu/emu.cpp
+
+build/libnpgen_host.so: $(CSRC)/emu/npgen_host.cpp $(HDRS)
+	@mkdir -p build
+	$(CXX_HOST) -std=c++20 -O2 -g -fPIC -shared -ffp-contract=off -fno-fast-math \
+		-Wall -Iinclude -o $@ $(CSRC)/emu/npgen_host.cpp -lm
 
 clean:
 	rm -rf build $(LIBDIR) oracle/build

@@ -41,6 +41,7 @@ from .cost_model import (
     profile_prefill,
     transfer_time,
 )
+from .device_traces import DeviceTrace, DeviceTraceSet, gen_synthetic_batch
 from .engine import RunResult, SimulationStallError, run, scale_trace
 from .monitor import InstanceStats, MonitorSnapshot
 from .pools import LEGAL_EDGES

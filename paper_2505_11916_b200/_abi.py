@@ -238,3 +238,48 @@ def fnv_decision_hash(decisions: np.ndarray) -> int:
         h = ((h ^ w1) * prime) & mask
         h = ((h ^ w2) * prime) & mask
     return h
+
+
+# ---- include/arrow_traces.h (device workload generator) ----
+
+SYNTH_MAX_BURSTS = 16
+SYNTH_MAX_SEED_WORDS = 8
+SYNTH_OK, SYNTH_CAPACITY, SYNTH_OVERFLOW = range(3)
+
+SYNTH_DTYPE = np.dtype(
+    [
+        ("duration_s", np.float64),
+        ("base_rate", np.float64),
+        ("rate_max", np.float64),
+        ("gap_scale", np.float64),
+        ("input_log_mean", np.float64),
+        ("input_log_sigma", np.float64),
+        ("output_log_mean", np.float64),
+        ("output_log_sigma", np.float64),
+        ("max_input", np.int64),
+        ("max_output", np.int64),
+        ("n_bursts", np.int32),
+        ("n_seed_words", np.int32),
+        ("seed_words", np.uint32, (SYNTH_MAX_SEED_WORDS,)),
+        ("burst_start", np.float64, (SYNTH_MAX_BURSTS,)),
+        ("burst_duration", np.float64, (SYNTH_MAX_BURSTS,)),
+        ("burst_multiplier", np.float64, (SYNTH_MAX_BURSTS,)),
+        ("out_offset", np.int64),
+        ("capacity", np.int64),
+    ],
+    align=True,
+)
+
+SYNTH_RESULT_DTYPE = np.dtype(
+    [
+        ("count", np.int64),
+        ("status", np.int32),
+        ("reserved", np.int32),
+        ("first_arrival", np.float64),
+        ("last_arrival", np.float64),
+        ("max_kv", np.int64),
+        ("sum_input", np.int64),
+        ("sum_output", np.int64),
+    ],
+    align=True,
+)

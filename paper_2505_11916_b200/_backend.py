@@ -109,6 +109,14 @@ class DeviceBatch:
         if inputs:
             src.update(inputs)
         self.h2d_bytes = 0
+        ds = cb.device_set
+        if ds is not None:
+            # generated traces are read in place (device_traces.py)
+            if ds.device != self.device:
+                raise ValueError(f"traces were generated on {ds.device}, the batch runs on {self.device}")
+            for name in ("arrival", "input_len", "output_len"):
+                src.pop(name)
+                self.tensors[name] = getattr(ds, name)
         for name, arr in src.items():
             if arr is None:
                 continue

@@ -121,19 +121,72 @@ class TraceEntry:
     offset: int = 0
 
 
+class DeviceTraceEntry:
+    """A trace generated on the device (device_traces.DeviceTrace): it is
+    read by the kernel in place; host copies are made only on demand (full
+    per-request outputs, validation error messages)."""
+
+    def __init__(self, dt) -> None:
+        self.device = dt
+        self.offset = dt.offset
+        self.n = dt.n
+        self._host = None
+
+    def _arrays(self):
+        if self._host is None:
+            self._host = self.device.arrays()
+        return self._host
+
+    @property
+    def arrival(self) -> np.ndarray:
+        return self._arrays()[0]
+
+    @property
+    def input_len(self) -> np.ndarray:
+        return self._arrays()[1]
+
+    @property
+    def output_len(self) -> np.ndarray:
+        return self._arrays()[2]
+
+    @property
+    def ids(self) -> np.ndarray:
+        return np.arange(self.n, dtype=np.int64)
+
+
+def entry_len(entry) -> int:
+    return entry.n if isinstance(entry, DeviceTraceEntry) else len(entry.arrival)
+
+
 class TraceTable:
     """Concatenated traces; each distinct trace object is stored once and
-    shared (read-only, L2-resident on the device) by every scenario using it."""
+    shared (read-only, L2-resident on the device) by every scenario using it.
+    A table holds either host traces or device traces of one generated set
+    (which the kernel then reads in place)."""
 
     def __init__(self) -> None:
-        self.entries: list[TraceEntry] = []
+        self.entries: list = []
         self._by_key: dict[int, int] = {}
         self.total = 0
+        self.device_set = None
 
     def add(self, trace) -> int:
+        from .device_traces import DeviceTrace
+
         key = id(trace)
         if key in self._by_key:
             return self._by_key[key]
+        if isinstance(trace, DeviceTrace):
+            if self.entries and self.device_set is None or (
+                self.device_set is not None and trace.set is not self.device_set
+            ):
+                raise ValueError("a batch takes host traces or device traces of one generated set, not a mix")
+            self.device_set = trace.set
+            self.entries.append(DeviceTraceEntry(trace))
+            self._by_key[key] = len(self.entries) - 1
+            return len(self.entries) - 1
+        if self.device_set is not None:
+            raise ValueError("a batch takes host traces or device traces of one generated set, not a mix")
         if isinstance(trace, TraceEntry):
             entry = trace
         else:
@@ -147,6 +200,8 @@ class TraceTable:
         return len(self.entries) - 1
 
     def arrays(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+        if self.device_set is not None:
+            return None, None, None  # read in place from the generated set
         if not self.entries:
             z = np.zeros(1, dtype=np.float64)
             return z, np.ones(1, dtype=np.int32), np.ones(1, dtype=np.int32)
@@ -182,6 +237,11 @@ class CompiledBatch:
     @property
     def n(self) -> int:
         return len(self.scenarios)
+
+    @property
+    def device_set(self):
+        """The generated trace set the kernel reads in place (None: host traces)."""
+        return self.table.device_set
 
 
 def scenario_record(config: RunConfig, trace_offset: int, n: int, scale: float, stall_limit: int) -> np.void:
@@ -234,13 +294,17 @@ def compile_batch(scenarios: list[Scenario], stall_limit: int, validate: bool = 
     for k, sc in enumerate(scenarios):
         t = table.add(sc.trace)
         entry = table.entries[t]
-        n = len(entry.arrival)
+        n = entry_len(entry)
         cfg = sc.config
         # reference order: predictor fit and token cap (in _Simulation.__init__)
         # raise before trace validation (in _Simulation.run)
         recs[k] = scenario_record(cfg, entry.offset, n, sc.scale, stall_limit)
         if validate:
             vkey = (t, sc.scale, cfg.instance.kv_capacity_tokens)
+            if isinstance(entry, DeviceTraceEntry) and entry.device.max_kv <= cfg.instance.kv_capacity_tokens:
+                # generated traces are sorted with ids 0..n-1 by construction
+                # (traces.py:166-175); only the KV bound can fail
+                validated.add(vkey)
             if vkey not in validated:
                 scaled = entry.arrival * sc.scale if sc.scale != 1.0 else entry.arrival
                 validate_trace(scaled, entry.ids, entry.input_len, entry.output_len, cfg.instance.kv_capacity_tokens)
@@ -272,10 +336,14 @@ def dispatch_order(cb: CompiledBatch) -> np.ndarray:
     est = np.zeros(cb.n)
     for k in range(cb.n):
         e = cb.table.entries[cb.trace_index[k]]
-        n = len(e.arrival)
+        n = entry_len(e)
         if n < 2:
             continue
-        span = (float(e.arrival[-1]) - float(e.arrival[0])) * float(cb.scenarios["arrival_scale"][k])
+        if isinstance(e, DeviceTraceEntry):
+            first, last, total_out = e.device.first_arrival, e.device.last_arrival, float(e.device.sum_output)
+        else:
+            first, last, total_out = float(e.arrival[0]), float(e.arrival[-1]), float(e.output_len.sum())
+        span = (last - first) * float(cb.scenarios["arrival_scale"][k])
         per_inst = (n - 1) / max(span, 1e-9) / max(int(cb.scenarios["n_instances"][k]), 1)
-        est[k] = float(e.output_len.sum()) / (1.0 + per_inst)
+        est[k] = total_out / (1.0 + per_inst)
     return np.argsort(-est, kind="stable").astype(np.int32)

@@ -94,6 +94,8 @@ def gen_synthetic(params: SyntheticParams) -> list[TraceRequest]:
 
 def native_rate(trace: list[TraceRequest]) -> float:
     """(n - 1) / span, the reference rate for rescaling (traces.py:253-261)."""
+    if hasattr(trace, "native_rate"):  # device_traces.DeviceTrace: from its device-side summary
+        return trace.native_rate()
     if len(trace) < 2:
         raise ValueError("need at least 2 requests to define a rate")
     span = trace[-1].arrival - trace[0].arrival

@@ -85,3 +85,41 @@ def test_product_fails_loudly_without_gpu():
     trace = [arrow.TraceRequest(0, 0.0, 100, 4)]
     with pytest.raises(EvaluatorUnavailable):
         arrow.run(trace, arrow.default_run_config())
+
+
+TRACES_HEADER = H.ROOT / "include" / "arrow_traces.h"
+
+
+def test_traces_header_symbols_exported(lib):
+    text = TRACES_HEADER.read_text()
+    names = sorted(set(re.findall(r"^\s*int\s+(arrow_\w+)\s*\(", text, re.M)))
+    assert names == ["arrow_synth_layout", "arrow_synth_run"]
+    for name in names:
+        assert hasattr(lib, name), name
+
+
+def test_synth_layout_matches_python_mirrors(lib):
+    out = (ctypes.c_int64 * 64)()
+    lib.arrow_synth_layout.restype = ctypes.c_int
+    n = lib.arrow_synth_layout(out, 64)
+    vals = list(out[:n])
+    dts = [_abi.SYNTH_DTYPE, _abi.SYNTH_RESULT_DTYPE]
+    expected = [d.itemsize for d in dts]
+    for d in dts:
+        expected += [d.fields[f][1] for f in d.names]
+    assert vals == expected
+    text = TRACES_HEADER.read_text()
+    assert f"#define ARROW_SYNTH_MAX_BURSTS {_abi.SYNTH_MAX_BURSTS}" in text
+    assert f"#define ARROW_SYNTH_MAX_SEED_WORDS {_abi.SYNTH_MAX_SEED_WORDS}" in text
+
+
+def test_generator_fails_loudly_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    import paper_2505_11916_b200 as arrow
+    from paper_2505_11916_b200._backend import EvaluatorUnavailable
+
+    with pytest.raises(EvaluatorUnavailable):
+        arrow.gen_synthetic_batch([arrow.SyntheticParams(10.0, 1.0, 5.0, 0.5, 4.0, 0.5)])
