@@ -11,7 +11,7 @@ LIBDIR := $(PKG)/lib
 LIB := $(LIBDIR)/libarrow_sim.so
 HDRS := include/arrow_sim.h include/arrow_traces.h $(CSRC)/sim_core.cuh $(CSRC)/warp.cuh \
 	$(CSRC)/npgen.cuh $(CSRC)/npgen_tables.h
-SRCS := $(CSRC)/arrow_sim.cu $(CSRC)/traces.cu
+SRCS := $(CSRC)/arrow_sim.cu $(CSRC)/traces.cu $(CSRC)/stats.cu
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -fmad=false -prec-div=true -Xptxas -v \
 	-Xcompiler -fPIC,-ffp-contract=off -Iinclude -I$(CSRC) --shared
 

@@ -78,6 +78,62 @@ int arrow_synth_run(const arrow_synth_t* specs, int32_t n_traces, double* arriva
  * offset in declaration order.  Returns the number of values. */
 int arrow_synth_layout(int64_t* out, int cap);
 
+/* ---- trace statistics (§8(f) rank 4) ------------------------------------
+ * Replaces the per-request scan of
+ *     pdsim.traces.trace_stats(trace, bucket_s)            traces.py:202-250
+ * with one streaming pass over the SoA trace (16 B per request): per-bucket
+ * request / input / output totals (bucket = int(arrival // bucket_s) with
+ * CPython's float floor division), first/last arrival with Python min/max
+ * tie semantics, exact integer moments for the Pearson r, and exact
+ * histograms of the lengths for np.percentile's order statistics.  The host
+ * turns these into TraceStats with the reference's own formulas. */
+
+#define ARROW_STATS_HIST_BINS 16384   /* lengths 1..16384 counted exactly in the scan */
+
+typedef struct arrow_stats_partial {  /* one per block; merged on the host */
+  double min_arrival;         /* NaN: block saw nothing */
+  double max_arrival;
+  int64_t count;              /* requests counted into buckets */
+  int64_t sum_x, sum_y;       /* x = input_len, y = output_len (bucketed requests) */
+  uint64_t sxx_lo, sxx_hi;    /* 128-bit sums of x*x, y*y, x*y */
+  uint64_t syy_lo, syy_hi;
+  uint64_t sxy_lo, sxy_hi;
+  int32_t min_x, max_x, min_y, max_y;
+  int64_t over_x, over_y;     /* lengths outside 1..ARROW_STATS_HIST_BINS */
+  int64_t out_of_window;      /* requests whose bucket fell outside [bucket_lo, bucket_lo + n_buckets) */
+} arrow_stats_partial_t;
+
+typedef struct arrow_stats_args {
+  const double* arrival;
+  const int32_t* input_len;
+  const int32_t* output_len;
+  int64_t n;
+  double bucket_s;            /* > 0 */
+  int64_t bucket_lo;          /* int(first // bucket_s), |bucket_lo| < 2^53 */
+  int64_t n_buckets;          /* hi - lo + 1 */
+  int64_t* bucket_requests;   /* [n_buckets] each, zeroed by arrow_stats_run */
+  int64_t* bucket_input;
+  int64_t* bucket_output;
+  uint32_t* hist_x;           /* [ARROW_STATS_HIST_BINS], bin v - 1; zeroed by arrow_stats_run */
+  uint32_t* hist_y;
+  arrow_stats_partial_t* partials;
+  int32_t n_partials;         /* grid size; arrow_stats_grid() gives the preferred value */
+  int32_t reserved;
+} arrow_stats_args_t;
+
+/* Preferred number of partials (blocks) for n requests on the current device. */
+int arrow_stats_grid(int64_t n, int32_t* n_partials);
+
+int arrow_stats_run(const arrow_stats_args_t* args, void* stream);
+
+/* Radix step for order statistics beyond the exact bins: counts values v of
+ * [values, values + n) with lo <= v < hi into bins[(v - lo) >> shift]
+ * (bins zeroed here, n_bins = ((hi - lo - 1) >> shift) + 1). */
+int arrow_stats_hist(const int32_t* values, int64_t n, int64_t lo, int64_t hi, int32_t shift, uint32_t* bins,
+                     int64_t n_bins, void* stream);
+
+int arrow_stats_layout(int64_t* out, int cap);
+
 #ifdef __cplusplus
 }
 #endif

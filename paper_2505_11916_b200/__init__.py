@@ -54,6 +54,7 @@ from .report import (
     sweep_max_rate,
     write_outputs,
 )
+from .stats import BucketStats, TraceStats, trace_stats
 from .sweep import evaluate_scenarios
 from .traces import (
     BurstEpisode,

@@ -1,0 +1,472 @@
+// stats.cu — trace statistics scan + C-ABI (include/arrow_traces.h).
+//
+// trace_stats (traces.py:202-250) is a pure scan: every request is read once
+// (arrival f64, input i32, output i32 = 16 B) and folded into
+//   * per-bucket totals, bucket = int(arrival // bucket_s) (CPython float
+//     floor division, reproduced exactly).  Each warp owns one contiguous
+//     range of the trace and keeps per-lane running totals for its current
+//     bucket; only when the bucket changes are they warp-reduced and added
+//     to HBM with three atomics.  A sorted trace therefore costs a handful of
+//     register adds per request and one flush per bucket boundary per warp;
+//     slices straddling buckets (or unsorted traces) fall back to
+//     __match_any_sync-grouped atomics;
+//   * exact histograms of the lengths 1..16384 in shared memory (flushed
+//     once per block) -> np.percentile's order statistics;
+//   * exact 64/128-bit integer moments (x^2, y^2, xy) -> the Pearson r;
+//   * min / max arrival.  (Python's min/max return the first of equal
+//     values, which differs only in the sign of a zero; no TraceStats field
+//     can observe it: the duration of an all-zero trace is z - z = +0.0.)
+// One persistent block per SM (the 128 KB histogram fills its shared
+// memory), 16 warps streaming 256-request chunks: every lane issues 24
+// independent coalesced loads before using any.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "arrow_traces.h"
+
+namespace {
+
+constexpr int kStatsThreads = 512;
+constexpr int kPer = 4;                 // requests per lane per chunk (x2 buffers in flight)
+constexpr int kChunk = 32 * kPer;
+constexpr int kWarps = kStatsThreads / 32;
+constexpr int kBins = ARROW_STATS_HIST_BINS;
+constexpr uint32_t FULL = 0xffffffffu;
+
+// CPython float_floor_div (Objects/floatobject.c, _float_div_mod), general path.
+__device__ __noinline__ double py_floordiv(double vx, double wx) {
+  double mod = fmod(vx, wx);
+  double div = (vx - mod) / wx;
+  if (mod != 0.0) {
+    if ((wx < 0) != (mod < 0)) div -= 1.0;
+  }
+  double fd;
+  if (div != 0.0) {
+    fd = floor(div);
+    if (div - fd > 0.5) fd += 1.0;
+  } else {
+    fd = copysign(0.0, vx / wx);
+  }
+  return fd;
+}
+
+// Fast path of the same: for vx >= 0, wx > 0 and a quotient below 2^50,
+// CPython returns trunc() of the EXACT quotient (fmod is exact, vx - mod =
+// m*wx rounds by at most 2^-53 relative, the division adds 2^-53, and the
+// final snap to the nearest integer absorbs both while m < 2^51).  That
+// integer is found without fmod's bit-serial loop: floor(vx * (1/wx)) is
+// within one of it and exact-sign FMA residuals vx - m*wx correct it.
+// ok = false sends the caller to py_floordiv.
+__device__ __forceinline__ double floordiv_fast(double vx, double wx, double inv, bool& ok) {
+  const double q = vx * inv;
+  ok = vx >= 0.0 && q < 0x1p50;
+  double m = floor(q);
+  if (fma(-m, wx, vx) < 0.0)
+    m -= 1.0;
+  else if (fma(-(m + 1.0), wx, vx) >= 0.0)
+    m += 1.0;
+  return m;
+}
+
+struct U128 {
+  uint64_t lo, hi;
+  __device__ __forceinline__ void add(uint64_t v) {
+    lo += v;
+    hi += (lo < v) ? 1u : 0u;
+  }
+  __device__ __forceinline__ void add(U128 o) {
+    lo += o.lo;
+    hi += o.hi + ((lo < o.lo) ? 1u : 0u);
+  }
+};
+
+struct Acc {
+  double tmin, tmax;
+  int64_t count, sx, sy, over_x, over_y, oow;
+  U128 sxx, syy, sxy;
+  int32_t mnx, mxx, mny, mxy;
+
+  __device__ void init() {
+    tmin = INFINITY;
+    tmax = -INFINITY;
+    count = sx = sy = over_x = over_y = oow = 0;
+    sxx = syy = sxy = U128{0, 0};
+    mnx = mny = INT32_MAX;
+    mxx = mxy = INT32_MIN;
+  }
+  __device__ void merge(const Acc& o) {
+    tmin = fmin(tmin, o.tmin);
+    tmax = fmax(tmax, o.tmax);
+    count += o.count;
+    sx += o.sx;
+    sy += o.sy;
+    over_x += o.over_x;
+    over_y += o.over_y;
+    oow += o.oow;
+    sxx.add(o.sxx);
+    syy.add(o.syy);
+    sxy.add(o.sxy);
+    mnx = min(mnx, o.mnx);
+    mxx = max(mxx, o.mxx);
+    mny = min(mny, o.mny);
+    mxy = max(mxy, o.mxy);
+  }
+};
+
+template <class T>
+__device__ __forceinline__ T shfl_down(T v, int d) {
+  return __shfl_down_sync(FULL, v, d);
+}
+
+__device__ void warp_merge(Acc& a) {
+  for (int d = 16; d > 0; d >>= 1) {
+    Acc o;
+    o.tmin = shfl_down(a.tmin, d);
+    o.tmax = shfl_down(a.tmax, d);
+    o.count = shfl_down(a.count, d);
+    o.sx = shfl_down(a.sx, d);
+    o.sy = shfl_down(a.sy, d);
+    o.over_x = shfl_down(a.over_x, d);
+    o.over_y = shfl_down(a.over_y, d);
+    o.oow = shfl_down(a.oow, d);
+    o.sxx = U128{shfl_down(a.sxx.lo, d), shfl_down(a.sxx.hi, d)};
+    o.syy = U128{shfl_down(a.syy.lo, d), shfl_down(a.syy.hi, d)};
+    o.sxy = U128{shfl_down(a.sxy.lo, d), shfl_down(a.sxy.hi, d)};
+    o.mnx = shfl_down(a.mnx, d);
+    o.mxx = shfl_down(a.mxx, d);
+    o.mny = shfl_down(a.mny, d);
+    o.mxy = shfl_down(a.mxy, d);
+    a.merge(o);
+  }
+}
+
+__device__ __forceinline__ uint64_t warp_sum(uint64_t v) {
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
+  return v;
+}
+
+// Per-lane running totals of the warp's current bucket.
+struct Run {
+  double f, f1;      // bucket (as the floor-division double) and f + 1, warp-uniform; NaN = none
+  uint32_t c;        // requests
+  uint64_t x, y;     // input / output tokens
+
+  __device__ void flush(const arrow_stats_args_t& A, Acc& acc, double lo_d, int lane) {
+    const uint64_t sc = warp_sum(c), sx = warp_sum(x), sy = warp_sum(y);
+    if (lane == 0 && sc) {
+      const int64_t b = (int64_t)(f - lo_d);
+      atomicAdd((unsigned long long*)&A.bucket_requests[b], (unsigned long long)sc);
+      atomicAdd((unsigned long long*)&A.bucket_input[b], (unsigned long long)sx);
+      atomicAdd((unsigned long long*)&A.bucket_output[b], (unsigned long long)sy);
+      acc.count += (int64_t)sc;
+      acc.sx += (int64_t)sx;
+      acc.sy += (int64_t)sy;
+    }
+    c = 0;
+    x = y = 0;
+  }
+};
+
+// Lanes holding the same bucket add their totals with one atomic per bucket.
+__device__ __forceinline__ void bucket_add(const arrow_stats_args_t& A, Acc& acc, int64_t b, int32_t x, int32_t y,
+                                           int lane) {
+  const unsigned long long key = (unsigned long long)b;
+  const uint32_t peers = __match_any_sync(FULL, key);
+  if (b < 0) return;
+  const uint32_t ux = (uint32_t)x, uy = (uint32_t)y;
+  const uint64_t sx = (uint64_t)__reduce_add_sync(peers, ux & 0xffffu) +
+                      ((uint64_t)__reduce_add_sync(peers, ux >> 16) << 16);
+  const uint64_t sy = (uint64_t)__reduce_add_sync(peers, uy & 0xffffu) +
+                      ((uint64_t)__reduce_add_sync(peers, uy >> 16) << 16);
+  if (lane == __ffs(peers) - 1) {
+    atomicAdd((unsigned long long*)&A.bucket_requests[b], (unsigned long long)__popc(peers));
+    atomicAdd((unsigned long long*)&A.bucket_input[b], (unsigned long long)sx);
+    atomicAdd((unsigned long long*)&A.bucket_output[b], (unsigned long long)sy);
+    acc.count += __popc(peers);
+    acc.sx += (int64_t)sx;
+    acc.sy += (int64_t)sy;
+  }
+}
+
+// A warp's chunk of 32*kPer requests held in registers.
+struct Chunk {
+  double t[kPer];
+  int32_t x[kPer], y[kPer];
+};
+
+__device__ __forceinline__ void load_chunk(const arrow_stats_args_t& A, Chunk& c, int64_t base, int64_t end,
+                                           int lane) {
+#pragma unroll
+  for (int k = 0; k < kPer; k++) {
+    const int64_t i = base + lane + 32 * k;
+    const bool v = i < end;
+    c.t[k] = v ? __ldcs(A.arrival + i) : 0.0;
+    c.x[k] = v ? __ldcs(A.input_len + i) : 0;
+    c.y[k] = v ? __ldcs(A.output_len + i) : 0;
+  }
+}
+
+// Fold one chunk [base, base + 32*kPer) (requests at or past `end` are
+// padding; kFull: none are).  Lengths below 2^29 keep x^2, y^2, xy sums of
+// one chunk inside 64 bits, so the 128-bit moments take one carry per chunk.
+template <bool kFull>
+__device__ __forceinline__ void fold_chunk(const arrow_stats_args_t& A, Acc& acc, Run& run, uint32_t* hist,
+                                           const Chunk& c, int64_t base, int64_t end, int lane, double lo_d,
+                                           double hi_d, double inv_b) {
+  const double w = A.bucket_s;
+  uint64_t qxx = 0, qyy = 0, qxy = 0;
+  uint32_t big = 0;
+#pragma unroll
+  for (int k = 0; k < kPer; k++) {
+    const bool v = kFull || base + lane + 32 * k < end;
+    const double t = c.t[k];
+    const int32_t x = c.x[k], y = c.y[k];
+    // Still in the run's bucket F?  For t >= 0 the bucket is trunc(t / w)
+    // (see floordiv_fast), so t is in F iff F*w <= t < (F+1)*w, decided
+    // exactly by the signs of two FMA residuals.
+    const bool in_run = fma(-run.f, w, t) >= 0.0 && fma(-run.f1, w, t) < 0.0;
+    if (__all_sync(FULL, !v || in_run)) {
+      run.c += v ? 1u : 0u;
+      run.x += (uint32_t)x;  // 0 on padding lanes
+      run.y += (uint32_t)y;
+    } else {
+      bool ok;
+      double f = floordiv_fast(t, w, inv_b, ok);
+      if (v && !ok) f = py_floordiv(t, w);
+      const bool inwin = f >= lo_d && f < hi_d;
+      const double f0 = __shfl_sync(FULL, f, 0);
+      if (__all_sync(FULL, !v || (ok && inwin && f == f0))) {
+        // the whole slice is in one new bucket: restart the run there
+        run.flush(A, acc, lo_d, lane);
+        run.f = f0;
+        run.f1 = f0 + 1.0;
+        run.c = v ? 1u : 0u;
+        run.x = (uint32_t)x;
+        run.y = (uint32_t)y;
+      } else {
+        const int64_t b = (v && inwin) ? (int64_t)(f - lo_d) : -1;
+        if (v && !inwin) acc.oow++;
+        bucket_add(A, acc, b, x, y, lane);
+      }
+    }
+    if (v) {
+      acc.tmin = t < acc.tmin ? t : acc.tmin;  // arrivals are never NaN
+      acc.tmax = t > acc.tmax ? t : acc.tmax;
+      acc.mnx = min(acc.mnx, x);
+      acc.mxx = max(acc.mxx, x);
+      acc.mny = min(acc.mny, y);
+      acc.mxy = max(acc.mxy, y);
+      if (x >= 1 && x <= kBins)
+        atomicAdd(&hist[x - 1], 1u);
+      else
+        acc.over_x++;
+      if (y >= 1 && y <= kBins)
+        atomicAdd(&hist[kBins + y - 1], 1u);
+      else
+        acc.over_y++;
+    }
+    const uint64_t ux = (uint32_t)x, uy = (uint32_t)y;
+    big |= (uint32_t)x | (uint32_t)y;
+    qxx += ux * ux;
+    qyy += uy * uy;
+    qxy += ux * uy;
+  }
+  if (big < (1u << 29)) {
+    acc.sxx.add(qxx);
+    acc.syy.add(qyy);
+    acc.sxy.add(qxy);
+  } else {  // huge lengths: redo this chunk's moments with a carry per term
+#pragma unroll
+    for (int k = 0; k < kPer; k++) {
+      const uint64_t ux = (uint32_t)c.x[k], uy = (uint32_t)c.y[k];
+      acc.sxx.add(ux * ux);
+      acc.syy.add(uy * uy);
+      acc.sxy.add(ux * uy);
+    }
+  }
+}
+
+__device__ __forceinline__ void fold(const arrow_stats_args_t& A, Acc& acc, Run& run, uint32_t* hist,
+                                     const Chunk& c, int64_t base, int64_t end, int lane, double lo_d, double hi_d,
+                                     double inv_b) {
+  if (base + kChunk <= end)
+    fold_chunk<true>(A, acc, run, hist, c, base, end, lane, lo_d, hi_d, inv_b);
+  else
+    fold_chunk<false>(A, acc, run, hist, c, base, end, lane, lo_d, hi_d, inv_b);
+}
+
+__global__ void __launch_bounds__(kStatsThreads, 1) arrow_stats_kernel(const arrow_stats_args_t A) {
+  extern __shared__ uint32_t hist[];  // [2][kBins]
+  __shared__ Acc red[kWarps];
+  for (int i = threadIdx.x; i < 2 * kBins; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  Acc acc;
+  acc.init();
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
+  Run run{nan, nan, 0, 0, 0};
+  const double lo_d = (double)A.bucket_lo;
+  const double hi_d = lo_d + (double)A.n_buckets;  // exclusive
+  const double inv_b = 1.0 / A.bucket_s;
+  // warp w streams the contiguous range [w * per, (w + 1) * per)
+  const int64_t n = A.n;
+  const int64_t warps = (int64_t)gridDim.x * kWarps;
+  const int64_t per = ((n + warps - 1) / warps + kChunk - 1) / kChunk * kChunk;
+  const int64_t w = (int64_t)blockIdx.x * kWarps + warp;
+  const int64_t begin = w * per;
+  const int64_t end = min(n, begin + per);
+  // software pipeline: the next chunk's loads are in flight while this
+  // chunk is folded (two register buffers, ping-pong)
+  Chunk c0, c1;
+  int64_t base = begin;
+  if (base < end) load_chunk(A, c0, base, end, lane);
+  while (base < end) {
+    const int64_t b1 = base + kChunk;
+    if (b1 < end) load_chunk(A, c1, b1, end, lane);
+    fold(A, acc, run, hist, c0, base, end, lane, lo_d, hi_d, inv_b);
+    if (b1 >= end) break;
+    const int64_t b2 = b1 + kChunk;
+    if (b2 < end) load_chunk(A, c0, b2, end, lane);
+    fold(A, acc, run, hist, c1, b1, end, lane, lo_d, hi_d, inv_b);
+    base = b2;
+  }
+  run.flush(A, acc, lo_d, lane);
+  warp_merge(acc);
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  for (int i = threadIdx.x; i < kBins; i += blockDim.x) {
+    if (hist[i]) atomicAdd(&A.hist_x[i], hist[i]);
+    if (hist[kBins + i]) atomicAdd(&A.hist_y[i], hist[kBins + i]);
+  }
+  if (threadIdx.x == 0) {
+    Acc a = red[0];
+    for (int q = 1; q < kWarps; q++) a.merge(red[q]);
+    arrow_stats_partial_t p;
+    p.min_arrival = a.count ? a.tmin : __longlong_as_double(0x7ff8000000000000ll);
+    p.max_arrival = a.count ? a.tmax : __longlong_as_double(0x7ff8000000000000ll);
+    p.count = a.count;
+    p.sum_x = a.sx;
+    p.sum_y = a.sy;
+    p.sxx_lo = a.sxx.lo;
+    p.sxx_hi = a.sxx.hi;
+    p.syy_lo = a.syy.lo;
+    p.syy_hi = a.syy.hi;
+    p.sxy_lo = a.sxy.lo;
+    p.sxy_hi = a.sxy.hi;
+    p.min_x = a.mnx;
+    p.max_x = a.mxx;
+    p.min_y = a.mny;
+    p.max_y = a.mxy;
+    p.over_x = a.over_x;
+    p.over_y = a.over_y;
+    p.out_of_window = a.oow;
+    A.partials[blockIdx.x] = p;
+  }
+}
+
+__global__ void arrow_stats_hist_kernel(const int32_t* __restrict__ values, int64_t n, int64_t lo, int64_t hi,
+                                        int32_t shift, uint32_t* __restrict__ bins) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t v = __ldcs(values + i);
+    if (v >= lo && v < hi) atomicAdd(&bins[(v - lo) >> shift], 1u);
+  }
+}
+
+int sm_count() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 1;
+  return sms > 0 ? sms : 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+int arrow_stats_grid(int64_t n, int32_t* n_partials) {
+  const int64_t chunks = (n + kPer * kStatsThreads - 1) / (kPer * kStatsThreads);
+  const int64_t g = chunks < sm_count() ? chunks : sm_count();
+  *n_partials = (int32_t)(g < 1 ? 1 : g);
+  return 0;
+}
+
+int arrow_stats_run(const arrow_stats_args_t* a, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t smem = 2 * kBins * sizeof(uint32_t);
+  cudaError_t e = cudaFuncSetAttribute(arrow_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  if (a->n_buckets > 0) {
+    const size_t nb = (size_t)a->n_buckets * sizeof(int64_t);
+    if ((e = cudaMemsetAsync(a->bucket_requests, 0, nb, s)) != cudaSuccess) return (int)e;
+    if ((e = cudaMemsetAsync(a->bucket_input, 0, nb, s)) != cudaSuccess) return (int)e;
+    if ((e = cudaMemsetAsync(a->bucket_output, 0, nb, s)) != cudaSuccess) return (int)e;
+  }
+  if ((e = cudaMemsetAsync(a->hist_x, 0, kBins * sizeof(uint32_t), s)) != cudaSuccess) return (int)e;
+  if ((e = cudaMemsetAsync(a->hist_y, 0, kBins * sizeof(uint32_t), s)) != cudaSuccess) return (int)e;
+  if (a->n_partials < 1) return (int)cudaErrorInvalidValue;
+  arrow_stats_kernel<<<a->n_partials, kStatsThreads, smem, s>>>(*a);
+  return (int)cudaGetLastError();
+}
+
+int arrow_stats_hist(const int32_t* values, int64_t n, int64_t lo, int64_t hi, int32_t shift, uint32_t* bins,
+                     int64_t n_bins, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(bins, 0, (size_t)n_bins * sizeof(uint32_t), s);
+  if (e != cudaSuccess) return (int)e;
+  if (n <= 0) return 0;
+  const int blocks = 4 * sm_count();
+  arrow_stats_hist_kernel<<<blocks, 512, 0, s>>>(values, n, lo, hi, shift, bins);
+  return (int)cudaGetLastError();
+}
+
+int arrow_stats_layout(int64_t* out, int cap) {
+  int64_t v[64];
+  int n = 0;
+#define SZ(T) v[n++] = (int64_t)sizeof(T)
+#define OFF(T, f) v[n++] = (int64_t)offsetof(T, f)
+  SZ(arrow_stats_partial_t);
+  SZ(arrow_stats_args_t);
+  OFF(arrow_stats_partial_t, min_arrival);
+  OFF(arrow_stats_partial_t, max_arrival);
+  OFF(arrow_stats_partial_t, count);
+  OFF(arrow_stats_partial_t, sum_x);
+  OFF(arrow_stats_partial_t, sum_y);
+  OFF(arrow_stats_partial_t, sxx_lo);
+  OFF(arrow_stats_partial_t, sxx_hi);
+  OFF(arrow_stats_partial_t, syy_lo);
+  OFF(arrow_stats_partial_t, syy_hi);
+  OFF(arrow_stats_partial_t, sxy_lo);
+  OFF(arrow_stats_partial_t, sxy_hi);
+  OFF(arrow_stats_partial_t, min_x);
+  OFF(arrow_stats_partial_t, max_x);
+  OFF(arrow_stats_partial_t, min_y);
+  OFF(arrow_stats_partial_t, max_y);
+  OFF(arrow_stats_partial_t, over_x);
+  OFF(arrow_stats_partial_t, over_y);
+  OFF(arrow_stats_partial_t, out_of_window);
+  OFF(arrow_stats_args_t, arrival);
+  OFF(arrow_stats_args_t, input_len);
+  OFF(arrow_stats_args_t, output_len);
+  OFF(arrow_stats_args_t, n);
+  OFF(arrow_stats_args_t, bucket_s);
+  OFF(arrow_stats_args_t, bucket_lo);
+  OFF(arrow_stats_args_t, n_buckets);
+  OFF(arrow_stats_args_t, bucket_requests);
+  OFF(arrow_stats_args_t, bucket_input);
+  OFF(arrow_stats_args_t, bucket_output);
+  OFF(arrow_stats_args_t, hist_x);
+  OFF(arrow_stats_args_t, hist_y);
+  OFF(arrow_stats_args_t, partials);
+  OFF(arrow_stats_args_t, n_partials);
+  OFF(arrow_stats_args_t, reserved);
+#undef SZ
+#undef OFF
+  for (int i = 0; i < n && i < cap; i++) out[i] = v[i];
+  return n;
+}
+
+}  // extern "C"

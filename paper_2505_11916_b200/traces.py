@@ -211,3 +211,7 @@ def save_trace(trace: list[TraceRequest], path: str | Path, fmt: str | None = No
             w.writerows([repr(float(r.arrival)), r.input_len, r.output_len] for r in ordered)
     else:
         raise TraceFormatError(f"unsupported trace format {fmt!r}")
+
+
+# traces.trace_stats (traces.py:181-250) lives with its GPU scan in stats.py
+from .stats import BucketStats, TraceStats, trace_stats  # noqa: E402,F401

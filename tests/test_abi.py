@@ -93,7 +93,8 @@ TRACES_HEADER = H.ROOT / "include" / "arrow_traces.h"
 def test_traces_header_symbols_exported(lib):
     text = TRACES_HEADER.read_text()
     names = sorted(set(re.findall(r"^\s*int\s+(arrow_\w+)\s*\(", text, re.M)))
-    assert names == ["arrow_synth_layout", "arrow_synth_run"]
+    assert names == ["arrow_stats_grid", "arrow_stats_hist", "arrow_stats_layout", "arrow_stats_run",
+                     "arrow_synth_layout", "arrow_synth_run"]
     for name in names:
         assert hasattr(lib, name), name
 
@@ -123,3 +124,20 @@ def test_generator_fails_loudly_without_gpu():
 
     with pytest.raises(EvaluatorUnavailable):
         arrow.gen_synthetic_batch([arrow.SyntheticParams(10.0, 1.0, 5.0, 0.5, 4.0, 0.5)])
+
+
+def test_stats_layout_matches_python_mirrors(lib):
+    from paper_2505_11916_b200 import stats as ST
+
+    out = (ctypes.c_int64 * 64)()
+    lib.arrow_stats_layout.restype = ctypes.c_int
+    n = lib.arrow_stats_layout(out, 64)
+    vals = list(out[:n])
+    expected = [ST.PARTIAL_DTYPE.itemsize, ctypes.sizeof(ST.StatsArgs)]
+    expected += [ST.PARTIAL_DTYPE.fields[f][1] for f in ST.PARTIAL_DTYPE.names]
+    expected += [getattr(ST.StatsArgs, f).offset for f, _ in ST.StatsArgs._fields_]
+    assert vals == expected
+    text = TRACES_HEADER.read_text()
+    assert f"#define ARROW_STATS_HIST_BINS {ST.HIST_BINS}" in text
+    for name in ("arrow_stats_grid", "arrow_stats_run", "arrow_stats_hist", "arrow_stats_layout"):
+        assert hasattr(lib, name), name
