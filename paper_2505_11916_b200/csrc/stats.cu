@@ -84,14 +84,14 @@ struct U128 {
 
 struct Acc {
   double tmin, tmax;
-  int64_t count, sx, sy, over_x, over_y, oow;
+  int64_t count, sx, sy, oow;
   U128 sxx, syy, sxy;
   int32_t mnx, mxx, mny, mxy;
 
   __device__ void init() {
     tmin = INFINITY;
     tmax = -INFINITY;
-    count = sx = sy = over_x = over_y = oow = 0;
+    count = sx = sy = oow = 0;
     sxx = syy = sxy = U128{0, 0};
     mnx = mny = INT32_MAX;
     mxx = mxy = INT32_MIN;
@@ -102,8 +102,6 @@ struct Acc {
     count += o.count;
     sx += o.sx;
     sy += o.sy;
-    over_x += o.over_x;
-    over_y += o.over_y;
     oow += o.oow;
     sxx.add(o.sxx);
     syy.add(o.syy);
@@ -128,8 +126,6 @@ __device__ void warp_merge(Acc& a) {
     o.count = shfl_down(a.count, d);
     o.sx = shfl_down(a.sx, d);
     o.sy = shfl_down(a.sy, d);
-    o.over_x = shfl_down(a.over_x, d);
-    o.over_y = shfl_down(a.over_y, d);
     o.oow = shfl_down(a.oow, d);
     o.sxx = U128{shfl_down(a.sxx.lo, d), shfl_down(a.sxx.hi, d)};
     o.syy = U128{shfl_down(a.syy.lo, d), shfl_down(a.syy.hi, d)};
@@ -140,6 +136,16 @@ __device__ void warp_merge(Acc& a) {
     o.mxy = shfl_down(a.mxy, d);
     a.merge(o);
   }
+}
+
+// hist[off + v - 1] += 1 for v in 1..kBins: one predicated red.shared on a
+// shared-window address (no generic-to-shared conversion per update).
+__device__ __forceinline__ void hist_inc(uint32_t hist_sa, int32_t v, int off) {
+  const uint32_t a = hist_sa + 4u * (uint32_t)(off + v - 1);
+  asm volatile(
+      "{\n .reg .pred p;\n setp.lt.u32 p, %1, %2;\n @p red.shared.add.u32 [%0], 1;\n}" ::"r"(a),
+      "r"((uint32_t)(v - 1)), "r"((uint32_t)kBins)
+      : "memory");
 }
 
 __device__ __forceinline__ uint64_t warp_sum(uint64_t v) {
@@ -216,6 +222,7 @@ __device__ __forceinline__ void fold_chunk(const arrow_stats_args_t& A, Acc& acc
                                            const Chunk& c, int64_t base, int64_t end, int lane, double lo_d,
                                            double hi_d, double inv_b) {
   const double w = A.bucket_s;
+  const uint32_t hist_sa = (uint32_t)__cvta_generic_to_shared(hist);
   uint64_t qxx = 0, qyy = 0, qxy = 0;
   uint32_t big = 0;
 #pragma unroll
@@ -258,14 +265,11 @@ __device__ __forceinline__ void fold_chunk(const arrow_stats_args_t& A, Acc& acc
       acc.mxx = max(acc.mxx, x);
       acc.mny = min(acc.mny, y);
       acc.mxy = max(acc.mxy, y);
-      if (x >= 1 && x <= kBins)
-        atomicAdd(&hist[x - 1], 1u);
-      else
-        acc.over_x++;
-      if (y >= 1 && y <= kBins)
-        atomicAdd(&hist[kBins + y - 1], 1u);
-      else
-        acc.over_y++;
+      // predicated shared-memory reductions on precomputed shared-window
+      // addresses (lengths outside 1..kBins are counted on the host as
+      // n - sum(bins))
+      hist_inc(hist_sa, x, 0);
+      hist_inc(hist_sa, y, kBins);
     }
     const uint64_t ux = (uint32_t)x, uy = (uint32_t)y;
     big |= (uint32_t)x | (uint32_t)y;
@@ -297,9 +301,60 @@ __device__ __forceinline__ void fold(const arrow_stats_args_t& A, Acc& acc, Run&
     fold_chunk<false>(A, acc, run, hist, c, base, end, lane, lo_d, hi_d, inv_b);
 }
 
+// ---- TMA bulk-copy pipeline (cp.async.bulk + mbarrier), one ring per warp ----
+
+constexpr int kStages = 3;
+struct Stage {  // one chunk of the SoA trace, as it sits in HBM
+  double t[kChunk];
+  int32_t x[kChunk], y[kChunk];
+};
+constexpr uint32_t kStageBytes = sizeof(Stage);
+static_assert(kStageBytes == 16 * kChunk, "stage = 16 B per request");
+constexpr size_t kHistBytes = 2 * kBins * sizeof(uint32_t);
+constexpr size_t kSmemBytes = kHistBytes + (size_t)kWarps * kStages * kStageBytes;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// Arm the stage's barrier for 16 B/request and start its three bulk copies.
+__device__ __forceinline__ void issue_stage(const arrow_stats_args_t& A, Stage* st, uint64_t* bar, int64_t base) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(kStageBytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(st->t)),
+      "l"(A.arrival + base), "r"((uint32_t)(kChunk * 8)), "r"(smem_u32(bar))
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(st->x)),
+      "l"(A.input_len + base), "r"((uint32_t)(kChunk * 4)), "r"(smem_u32(bar))
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(st->y)),
+      "l"(A.output_len + base), "r"((uint32_t)(kChunk * 4)), "r"(smem_u32(bar))
+      : "memory");
+}
+
 __global__ void __launch_bounds__(kStatsThreads, 1) arrow_stats_kernel(const arrow_stats_args_t A) {
-  extern __shared__ uint32_t hist[];  // [2][kBins]
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint32_t* hist = (uint32_t*)smem_raw;  // [2][kBins]
   __shared__ Acc red[kWarps];
+  __shared__ uint64_t bars[kWarps][kStages];
   for (int i = threadIdx.x; i < 2 * kBins; i += blockDim.x) hist[i] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -318,20 +373,63 @@ __global__ void __launch_bounds__(kStatsThreads, 1) arrow_stats_kernel(const arr
   const int64_t w = (int64_t)blockIdx.x * kWarps + warp;
   const int64_t begin = w * per;
   const int64_t end = min(n, begin + per);
-  // software pipeline: the next chunk's loads are in flight while this
-  // chunk is folded (two register buffers, ping-pong)
-  Chunk c0, c1;
-  int64_t base = begin;
-  if (base < end) load_chunk(A, c0, base, end, lane);
-  while (base < end) {
-    const int64_t b1 = base + kChunk;
-    if (b1 < end) load_chunk(A, c1, b1, end, lane);
-    fold(A, acc, run, hist, c0, base, end, lane, lo_d, hi_d, inv_b);
-    if (b1 >= end) break;
-    const int64_t b2 = b1 + kChunk;
-    if (b2 < end) load_chunk(A, c0, b2, end, lane);
-    fold(A, acc, run, hist, c1, b1, end, lane, lo_d, hi_d, inv_b);
-    base = b2;
+  const bool aligned = (((uintptr_t)A.arrival | (uintptr_t)A.input_len | (uintptr_t)A.output_len) & 15) == 0;
+  if (aligned) {
+    // Every full chunk of the warp's range streams HBM -> shared memory by
+    // TMA bulk copies through a kStages-deep ring (one elected lane issues,
+    // the mbarrier's transaction count says when the 16 B/request landed),
+    // so ~kStages chunks per warp are in flight while the lanes fold; only
+    // a partial last chunk is loaded through registers.
+    Stage* ring = (Stage*)(smem_raw + kHistBytes) + warp * kStages;
+    uint64_t* bar = bars[warp];
+    const int64_t nfull = (end > begin) ? (end - begin) / kChunk : 0;
+    if (lane == 0) {
+      for (int q = 0; q < kStages; q++) mbar_init(&bar[q]);
+      asm volatile("fence.mbarrier_init.release.cluster;\n fence.proxy.async.shared::cta;" ::: "memory");
+      for (int q = 0; q < kStages && q < nfull; q++) issue_stage(A, &ring[q], &bar[q], begin + (int64_t)q * kChunk);
+    }
+    __syncwarp();
+    for (int64_t j = 0; j < nfull; j++) {
+      const int q = (int)(j % kStages);
+      const uint32_t parity = (uint32_t)((j / kStages) & 1);
+      while (!mbar_try_wait(&bar[q], parity)) {
+      }
+      Chunk c;
+#pragma unroll
+      for (int k = 0; k < kPer; k++) {
+        c.t[k] = ring[q].t[lane + 32 * k];
+        c.x[k] = ring[q].x[lane + 32 * k];
+        c.y[k] = ring[q].y[lane + 32 * k];
+      }
+      __syncwarp();  // every lane has read the stage before it is refilled
+      if (lane == 0 && j + kStages < nfull) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_stage(A, &ring[q], &bar[q], begin + (j + kStages) * kChunk);
+      }
+      fold_chunk<true>(A, acc, run, hist, c, begin + j * kChunk, end, lane, lo_d, hi_d, inv_b);
+    }
+    const int64_t tail = begin + nfull * kChunk;
+    if (tail < end) {
+      Chunk c;
+      load_chunk(A, c, tail, end, lane);
+      fold_chunk<false>(A, acc, run, hist, c, tail, end, lane, lo_d, hi_d, inv_b);
+    }
+  } else {
+    // unaligned views: register double buffering (the next chunk's loads
+    // are in flight while this one is folded)
+    Chunk c0, c1;
+    int64_t base = begin;
+    if (base < end) load_chunk(A, c0, base, end, lane);
+    while (base < end) {
+      const int64_t b1 = base + kChunk;
+      if (b1 < end) load_chunk(A, c1, b1, end, lane);
+      fold(A, acc, run, hist, c0, base, end, lane, lo_d, hi_d, inv_b);
+      if (b1 >= end) break;
+      const int64_t b2 = b1 + kChunk;
+      if (b2 < end) load_chunk(A, c0, b2, end, lane);
+      fold(A, acc, run, hist, c1, b1, end, lane, lo_d, hi_d, inv_b);
+      base = b2;
+    }
   }
   run.flush(A, acc, lo_d, lane);
   warp_merge(acc);
@@ -360,8 +458,6 @@ __global__ void __launch_bounds__(kStatsThreads, 1) arrow_stats_kernel(const arr
     p.max_x = a.mxx;
     p.min_y = a.mny;
     p.max_y = a.mxy;
-    p.over_x = a.over_x;
-    p.over_y = a.over_y;
     p.out_of_window = a.oow;
     A.partials[blockIdx.x] = p;
   }
@@ -396,7 +492,7 @@ int arrow_stats_grid(int64_t n, int32_t* n_partials) {
 
 int arrow_stats_run(const arrow_stats_args_t* a, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  const size_t smem = 2 * kBins * sizeof(uint32_t);
+  const size_t smem = kSmemBytes;
   cudaError_t e = cudaFuncSetAttribute(arrow_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
   if (a->n_buckets > 0) {
@@ -445,8 +541,6 @@ int arrow_stats_layout(int64_t* out, int cap) {
   OFF(arrow_stats_partial_t, max_x);
   OFF(arrow_stats_partial_t, min_y);
   OFF(arrow_stats_partial_t, max_y);
-  OFF(arrow_stats_partial_t, over_x);
-  OFF(arrow_stats_partial_t, over_y);
   OFF(arrow_stats_partial_t, out_of_window);
   OFF(arrow_stats_args_t, arrival);
   OFF(arrow_stats_args_t, input_len);

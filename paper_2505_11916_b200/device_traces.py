@@ -103,7 +103,13 @@ def synth_record(params: SyntheticParams, out_offset: int, capacity: int) -> np.
 
 def _capacity(params: SyntheticParams) -> int:
     lam = expected_requests(params)
-    return int(lam + 10.0 * math.sqrt(lam) + 32)
+    return _round4(int(lam + 10.0 * math.sqrt(lam) + 32))
+
+
+def _round4(c: int) -> int:
+    """Slots per trace in multiples of 4 requests, so every trace's slice of
+    the SoA arrays starts 16-byte aligned (TMA bulk copies in stats.cu)."""
+    return (int(c) + 3) // 4 * 4
 
 
 _lib_ready = False
@@ -234,7 +240,7 @@ def gen_synthetic_batch(params_list, device=None, stream=None) -> DeviceTraceSet
         over = res["status"] == _abi.SYNTH_CAPACITY
         if not over.any():
             break
-        caps = [int(max(c, n)) for c, n in zip(caps, res["count"])]
+        caps = [_round4(max(c, n)) for c, n in zip(caps, res["count"])]
     for i, p in enumerate(params_list):
         r = res[i]
         if int(r["count"]) > 0:

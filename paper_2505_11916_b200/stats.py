@@ -52,8 +52,6 @@ PARTIAL_DTYPE = np.dtype(
         ("max_x", np.int32),
         ("min_y", np.int32),
         ("max_y", np.int32),
-        ("over_x", np.int64),
-        ("over_y", np.int64),
         ("out_of_window", np.int64),
     ],
     align=True,
@@ -302,8 +300,6 @@ def _merge(p: np.ndarray) -> dict:
         max_x=int(live["max_x"].max()),
         min_y=int(live["min_y"].min()),
         max_y=int(live["max_y"].max()),
-        over_x=int(live["over_x"].sum()),
-        over_y=int(live["over_y"].sum()),
         oow=int(live["out_of_window"].sum()),
     )
 
@@ -347,10 +343,11 @@ def _finish(lib, torch, d, res, bucket_s, device, stream) -> TraceStats:
         f = int(np.floor(v))
         ranks.update(k for k in (f, f + 1) if 0 <= k < n)
     ranks.add(n - 1)
-    osx = _order_stats(lib, torch, d.input_len, res["hist"][0], m["over_x"], m["max_x"], n, sorted(ranks), device,
-                       stream)
-    osy = _order_stats(lib, torch, d.output_len, res["hist"][1], m["over_y"], m["max_y"], n, sorted(ranks), device,
-                       stream)
+    # lengths outside the exact bins: n - sum(bins)
+    over_x = n - int(res["hist"][0].astype(np.int64).sum())
+    over_y = n - int(res["hist"][1].astype(np.int64).sum())
+    osx = _order_stats(lib, torch, d.input_len, res["hist"][0], over_x, m["max_x"], n, sorted(ranks), device, stream)
+    osy = _order_stats(lib, torch, d.output_len, res["hist"][1], over_y, m["max_y"], n, sorted(ranks), device, stream)
     return TraceStats(
         num_requests=n,
         duration_s=duration,
