@@ -209,6 +209,22 @@ def run_reference(args, rank: int, world: int) -> None:
     print(json.dumps(line))
 
 
+def measure_components() -> dict:
+    """The §8(f) kernels around the evaluator, each on its own (not part of
+    the headline step): the device workload generator (rank 3, 8 192 seeds
+    of the bundled bursty workload per launch) and the trace_stats scan
+    (rank 4, a 100 M-request trace resident in HBM, L2 flushed per launch),
+    with their CPU-reference rates on one host core for context."""
+    sys.path.insert(0, str(ROOT / "scripts"))
+    import bench_stats
+    import bench_traces
+
+    return {
+        "gen_synthetic": bench_traces.measure(8192, steps=5, warmup=2, cpu_sample=4),
+        "trace_stats": bench_stats.measure(100_000_000, steps=10, warmup=3, cpu_sample=100_000),
+    }
+
+
 def run_ours(args, rank: int, world: int) -> None:
     import torch
 
@@ -317,6 +333,9 @@ def run_ours(args, rank: int, world: int) -> None:
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_port_baseline(scenarios, 30.0, host_threads())
+    components = None
+    if rank == 0 and world == 1 and not args.no_components:
+        components = measure_components()
     if dist:
         dist.barrier()
     if rank == 0:
@@ -349,6 +368,7 @@ def run_ours(args, rank: int, world: int) -> None:
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
             "kernel_ms_per_launch": ms,
+            "components": components,
         }
         print(json.dumps(line))
     if dist:
@@ -363,6 +383,7 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-components", action="store_true")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

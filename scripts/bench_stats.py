@@ -39,15 +39,8 @@ def hbm_peak() -> tuple[float, str]:
     return 6547.5, "fallback"
 
 
-def main() -> None:
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--requests", type=int, default=200_000_000)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--bucket", type=float, default=60.0)
-    ap.add_argument("--cpu-sample", type=int, default=200_000)
-    args = ap.parse_args()
-
+def measure(requests: int, steps: int = 10, warmup: int = 3, bucket: float = 60.0, cpu_sample: int = 200_000) -> dict:
+    args = argparse.Namespace(requests=requests, steps=steps, warmup=warmup, bucket=bucket, cpu_sample=cpu_sample)
     import numpy as np
     import torch
 
@@ -103,14 +96,25 @@ def main() -> None:
     t0 = time.perf_counter()
     SO.trace_stats_arrays(sa, si, so, args.bucket)
     cpu_s = time.perf_counter() - t0
-    print(json.dumps({
+    return {
         "metric": "trace_stats requests/s", "value": n / (ms * 1e-3), "unit": "requests/s", "ms_per_scan": ms,
         "requests": n, "buckets": nb, "grid": grid.value,
         "roofline": {"bound": "hbm", "achieved": gbps, "peak": peak, "unit": "GB/s", "frac": gbps / peak,
                      "peak_source": src, "algorithmic_bytes_per_request": 16},
         "cpu_reference": {"value": k / cpu_s, "unit": "requests/s", "cores": 1,
                           "sample": f"first {k} requests, CPU restatement of traces.py:202-250"},
-    }))
+    }
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--requests", type=int, default=200_000_000)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--bucket", type=float, default=60.0)
+    ap.add_argument("--cpu-sample", type=int, default=200_000)
+    a = ap.parse_args()
+    print(json.dumps(measure(a.requests, a.steps, a.warmup, a.bucket, a.cpu_sample)))
 
 
 if __name__ == "__main__":

@@ -22,13 +22,8 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 
-def main() -> None:
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--seeds", type=int, default=8192)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=2)
-    ap.add_argument("--cpu-sample", type=int, default=8)
-    args = ap.parse_args()
+def measure(seeds: int, steps: int = 5, warmup: int = 2, cpu_sample: int = 8) -> dict:
+    args = argparse.Namespace(seeds=seeds, steps=steps, warmup=warmup, cpu_sample=cpu_sample)
 
     import ctypes
 
@@ -78,7 +73,7 @@ def main() -> None:
     for p in params[: args.cpu_sample]:
         n_cpu += len(arrow.gen_synthetic(p))
     cpu_s = time.perf_counter() - t0
-    print(json.dumps({
+    return {
         "metric": "generated requests/s",
         "value": total / (ms / 1e3),
         "unit": "requests/s",
@@ -88,7 +83,17 @@ def main() -> None:
         "achieved_GBps": bytes_per / (ms * 1e6),
         "cpu_reference": {"value": n_cpu / cpu_s, "unit": "requests/s", "cores": 1,
                           "sample": f"{args.cpu_sample} seeds, numpy host generator (the reference's algorithm)"},
-    }))
+    }
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--seeds", type=int, default=8192)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--cpu-sample", type=int, default=8)
+    a = ap.parse_args()
+    print(json.dumps(measure(a.seeds, a.steps, a.warmup, a.cpu_sample)))
 
 
 if __name__ == "__main__":
