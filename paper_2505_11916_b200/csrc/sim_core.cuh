@@ -1573,14 +1573,22 @@ struct Sim {
            !(I.mq_c > 0 && !I.mig_active && I.wd_c > 0);
   }
 
-  AS_HD uint64_t chain_loud_bound(const Inst& I, uint64_t limit) const {
+  // Lower bound on the completion time of the chain's first loud iteration
+  // (the one where the earliest running decode finishes and the queued
+  // migration's gate can open): busy_until + dur + ... + dur, `steps`
+  // additions each rounded to nearest.  Every partial sum is <= T (the
+  // closed form), so the accumulated rounding and the closed form's own are
+  // below (steps + 4) ulp(T) <= (steps + 4) T 2^-52: L <= the exact sum.
+  // Any lower bound keeps the burst exact (it only stops earlier); the
+  // closed form replaces a serially dependent addition loop of up to
+  // BURST_MAX steps per burst selection.
+  AS_HD uint64_t chain_loud_bound(const Inst& I) const {
     if (I.mq_c == 0 || I.mig_active) return ~0ull;
     const int steps = I.min_f - (I.it - 1);   // >= 1: the pending event itself is quiet
     const double dur = sc().b1 * (double)I.R + sc().b0;
-    const double tlim = okey_inv(limit);
-    double t = I.busy_until;
-    for (int i = 0; i < steps && t < tlim; i++) t = t + dur;
-    return tkey(t);
+    const double T = I.busy_until + (double)steps * dur;
+    const double L = T - (double)(steps + 4) * (T * 0x1p-52);
+    return tkey(L > I.busy_until ? L : I.busy_until);
   }
 
   // Returns true and the horizon (events with key < hz are run) when some
@@ -1628,7 +1636,7 @@ struct Sim {
 #pragma unroll
       for (int k = 0; k < IPL; k++)
         if (safe[k]) {
-          const uint64_t b = chain_loud_bound(st[k], cap);
+          const uint64_t b = chain_loud_bound(st[k]);
           if (b < loud) loud = b;
         }
       const uint32_t lhi = w.min_u32((uint32_t)(loud >> 32));

@@ -18,7 +18,10 @@
 
 namespace {
 
-constexpr int kGenThreads = 64;  // small blocks spread a few thousand traces over all 148 SMs
+#ifndef ARROW_GEN_THREADS
+#define ARROW_GEN_THREADS 128
+#endif
+constexpr int kGenThreads = ARROW_GEN_THREADS;
 
 __global__ void __launch_bounds__(kGenThreads) arrow_synth_kernel(const arrow_synth_t* __restrict__ specs, int n_traces,
                                                                   double* __restrict__ arrival,
