@@ -257,3 +257,13 @@ const char* arrow_sim_status_string(int status) {
 }
 
 }  // extern "C"
+
+#ifdef ARROW_PROF
+// Profiling build only (-DARROW_PROF): serial-step cycles by event kind per
+// scenario id (arrival, -, prefill-complete, -, tick, loud iteration,
+// migration, rescan), copied out after a launch.
+extern "C" int arrow_sim_prof(int64_t* out, int n) {
+  if (n > ARROW_PROF_MAX) n = ARROW_PROF_MAX;
+  return (int)cudaMemcpyFromSymbol(out, arrow_prof_cycles, (size_t)n * 16 * sizeof(int64_t));
+}
+#endif

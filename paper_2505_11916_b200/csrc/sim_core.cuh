@@ -48,6 +48,11 @@
   } while (0)
 #endif
 
+#if defined(ARROW_PROF) && defined(__CUDACC__)
+#define ARROW_PROF_MAX 4096
+__device__ int64_t arrow_prof_cycles[ARROW_PROF_MAX * 16];
+#endif
+
 namespace arrow {
 
 enum { EV_MIG = 0, EV_ITER = 1, EV_PREFILL = 2, EV_ARRIVAL = 3, EV_TICK = 4 };
@@ -141,6 +146,7 @@ struct Uniform {
   int64_t rr_p, rr_d;
   int64_t n_rounds, n_serial, n_bursts;
   int64_t cyc_serial, cyc_round, cyc_burst;   // profiling: SM cycles by step kind
+  int64_t cyc_kind[16];                       // ARROW_PROF: serial cycles by event kind, rescan, selection/execution
   uint64_t hash;
   uint32_t seq, tick_seq;
   int a;
@@ -168,6 +174,7 @@ struct WarpSmem {
   int bhead[MAX_INST];           // merge cursor (tie fallback)
   int blast[MAX_INST];           // its last event pushed a successor
   uint32_t bseq[MAX_INST];       // sequence of its head / final pending push
+  uint64_t bfinal[MAX_INST];     // key of its final pushing event (~0: none)
   int btie;
 };
 
@@ -256,6 +263,30 @@ AS_HD double quad(double a2, double a1, double a0, int len) {
 AS_HD int imin(int a, int b) { return a < b ? a : b; }
 
 // ------------------------------------------------------------- simulator --
+
+#ifdef ARROW_PROF
+#define PROF_CLOCK(var) const int64_t var = clock_now()
+#define PROF_ADD(field, since)                           \
+  do {                                                   \
+    const int64_t _now = clock_now();                    \
+    if (lane == 0) u().field += _now - (since);          \
+  } while (0)
+#define PROF_MARK(slot, since)                              \
+  do {                                                      \
+    const int64_t _now = clock_now();                       \
+    if (lane == 0) u().cyc_kind[slot] += _now - (since);    \
+  } while (0)
+#else
+#define PROF_CLOCK(var) \
+  do {                  \
+  } while (0)
+#define PROF_ADD(field, since) \
+  do {                         \
+  } while (0)
+#define PROF_MARK(slot, since) \
+  do {                         \
+  } while (0)
+#endif
 
 template <class W, int IPL>
 struct Sim {
@@ -1820,6 +1851,32 @@ struct Sim {
     return lo;
   }
 
+  // Entries of the sorted a[0..n) below x, and whether x occurs.  Chains are
+  // short (a few events): independent loads four at a time beat the
+  // dependent shared-memory loads of a binary search; long lists search.
+  static AS_HD int count_below_u64(const uint64_t* a, int n, uint64_t x, bool& eq) {
+    if (n > 16) {
+      const int lb = lower_bound_u64(a, n, x);
+      eq = lb < n && a[lb] == x;
+      return lb;
+    }
+    int c = 0;
+    bool e = false;
+    int j = 0;
+    for (; j + 4 <= n; j += 4) {
+      const uint64_t v0 = a[j], v1 = a[j + 1], v2 = a[j + 2], v3 = a[j + 3];
+      c += (int)(v0 < x) + (int)(v1 < x) + (int)(v2 < x) + (int)(v3 < x);
+      e = e || v0 == x || v1 == x || v2 == x || v3 == x;
+    }
+    for (; j < n; j++) {
+      const uint64_t v = a[j];
+      c += (int)(v < x);
+      e = e || v == x;
+    }
+    eq = e;
+    return c;
+  }
+
   AS_HD void run_burst(const bool safe[IPL], const Head& hz, int per, Head& h) {
     // segments: participant rank (slot-major, then lane) x per
     int rank[IPL];
@@ -1832,6 +1889,7 @@ struct Sim {
         base_rank += popc32(m);
       }
     }
+    PROF_CLOCK(pb0);
     int completed = 0, events = 0, pushes = 0;
     int lastp[IPL];
 #pragma unroll
@@ -1854,34 +1912,56 @@ struct Sim {
     const uint32_t base = u().seq;
     if (lane == 0) sm->btie = 0;
     w.sync();
-    // The final pending push of each chain gets the global counter value it
-    // would have had: base + pushes (all chains) ordered before it.  Pushes
-    // inside the burst belong to events already executed, so their own
-    // numbers are never compared again.  Exact time ties with another
-    // chain's event fall back to a sequential merge.
+    PROF_MARK(12, pb0);
+    PROF_CLOCK(pb1);
+    // Sequence numbers only order events with equal times, and the pushes
+    // inside a burst belong to events already executed: what the final
+    // pending push of each chain must carry is its order relative to the
+    // other chains' final pushes (by the time of the event that pushed it)
+    // and a value in [base, base + total pushes), above every earlier push
+    // and below every later one.  Rank among the finals gives exactly that;
+    // equal final times fall back to the sequential merge below, which
+    // reproduces the full (time, seq) order.
     int before[IPL];
+    uint64_t xlast[IPL];  // key of each chain's final (pending-push) event
 #pragma unroll
-    for (int k = 0; k < IPL; k++) before[k] = sm->bcount[st[k].id >= 0 ? st[k].id : 0] - 1;
+    for (int k = 0; k < IPL; k++) {
+      before[k] = 0;
+      xlast[k] = ~0ull;
+      if (st[k].id < 0) continue;
+      const int id = st[k].id;
+      if (safe[k] && lastp[k]) xlast[k] = sm->blist[sm->boff[id] + sm->bcount[id] - 1];
+      sm->bfinal[id] = xlast[k];
+    }
+    const int n_final = (int)w.add_u32((uint32_t)(
+        (IPL > 0 && safe[0] && lastp[0] ? 1 : 0) + (IPL > 1 && safe[IPL - 1] && lastp[IPL - 1] ? 1 : 0)));
+    w.sync();
+    bool tie_seen = false;
+    {
+      const int N = sc().n_instances;
 #pragma unroll
-    for (int kk = 0; kk < IPL; kk++) {
-      uint32_t m = w.ballot(safe[kk]);
-      while (m) {
-        const int j = ffs32(m);
-        m &= m - 1;
-        const int other = w.shfl(st[kk].id, j);
-        const uint64_t* lst = sm->blist + sm->boff[other];
-        const int n_o = sm->bcount[other];
-        const int last_o = sm->blast[other];
-#pragma unroll
-        for (int k = 0; k < IPL; k++) {
-          if (!safe[k] || !lastp[k] || st[k].id == other) continue;
-          const uint64_t x = sm->blist[sm->boff[st[k].id] + sm->bcount[st[k].id] - 1];
-          const int lb = lower_bound_u64(lst, n_o, x);
-          if (lb < n_o && lst[lb] == x) sm->btie = 1;
-          before[k] += lb - ((lb == n_o && !last_o) ? 1 : 0);
+      for (int k = 0; k < IPL; k++) {
+        if (!(safe[k] && lastp[k])) continue;
+        const uint64_t x = xlast[k];
+        int r = 0;
+        bool eq = false;
+        int i = 0;
+        for (; i + 4 <= N; i += 4) {
+          const uint64_t v0 = sm->bfinal[i], v1 = sm->bfinal[i + 1], v2 = sm->bfinal[i + 2], v3 = sm->bfinal[i + 3];
+          r += (int)(v0 < x) + (int)(v1 < x) + (int)(v2 < x) + (int)(v3 < x);
+          eq = eq || (v0 == x && i != st[k].id) || (v1 == x && i + 1 != st[k].id) ||
+               (v2 == x && i + 2 != st[k].id) || (v3 == x && i + 3 != st[k].id);
         }
+        for (; i < N; i++) {
+          const uint64_t v = sm->bfinal[i];
+          r += (int)(v < x);
+          eq = eq || (v == x && i != st[k].id);
+        }
+        before[k] = r;
+        tie_seen = tie_seen || eq;
       }
     }
+    if (tie_seen) sm->btie = 1;
     const uint32_t packed = w.add_u32((uint32_t)events | ((uint32_t)completed << 16));
     const uint32_t total_push = w.add_u32((uint32_t)pushes);
     w.sync();
@@ -1889,7 +1969,7 @@ struct Sim {
     if (!tie) {
 #pragma unroll
       for (int k = 0; k < IPL; k++)
-        if (safe[k] && lastp[k]) st[k].iter_seq = base + (uint32_t)before[k];
+        if (safe[k] && lastp[k]) st[k].iter_seq = base + total_push - (uint32_t)n_final + (uint32_t)before[k];
     } else {
       // sequential merge of all chains in (time, seq) order; bseq[i] holds
       // the sequence of chain i's current head event
@@ -1927,6 +2007,7 @@ struct Sim {
       for (int k = 0; k < IPL; k++)
         if (safe[k] && lastp[k]) st[k].iter_seq = sm->bseq[st[k].id];
     }
+    PROF_MARK(13, pb1);
     // a chain stopped at its migration bound leaves a loud pending event
     Head loud;
     loud.code = -1;
@@ -1963,6 +2044,8 @@ struct Sim {
     return U.a >= sc().n_requests && U.fifo_count == 0 && U.tick_active && U.completed < sc().n_requests;
   }
 
+
+
   AS_HD void simulate() {
     const int64_t limit = sc().stall_limit;
     Head h = full_scan();
@@ -1970,18 +2053,27 @@ struct Sim {
       bool part[IPL];
       Head hz;
       int per = 0;
-      const int64_t c0 = clock_now();
-      if (burst_select(h, hz, part, per)) {
+      PROF_CLOCK(c0);
+      const bool bsel = burst_select(h, hz, part, per);
+      PROF_MARK(8, c0);
+      if (bsel) {
+        PROF_CLOCK(cb);
         run_burst(part, hz, per, h);
-        if (lane == 0) u().cyc_burst += clock_now() - c0;
+        PROF_MARK(9, cb);
+        PROF_ADD(cyc_burst, c0);
         const int status = u().status;
         w.sync();
         if (status != ARROW_OK) return;
         continue;
       }
-      if (round_select(h, part)) {
+      PROF_CLOCK(cr);
+      const bool rsel = round_select(h, part);
+      PROF_MARK(10, cr);
+      if (rsel) {
+        PROF_CLOCK(cx);
         run_round(part, h);
-        if (lane == 0) u().cyc_round += clock_now() - c0;
+        PROF_MARK(11, cx);
+        PROF_ADD(cyc_round, c0);
         const int status = u().status;
         w.sync();
         if (status != ARROW_OK) return;
@@ -1997,6 +2089,9 @@ struct Sim {
         u().n_serial++;
         ATRACE("ev %d t=%.17g esp=%lld\n", ev, now, (long long)u().esp);
       });
+#ifdef ARROW_PROF
+      const int prof_kind = ev >= 1000 ? ev - 1000 : ((ev & 1) ? 5 : 6);
+#endif
       if (ev >= 1000) {
         int kind = ev - 1000;
         if (kind == EV_ARRIVAL) {
@@ -2068,8 +2163,15 @@ struct Sim {
         });
         return;
       }
+      PROF_CLOCK(c1);
       h = full_scan();
-      if (lane == 0) u().cyc_serial += clock_now() - c0;
+      PROF_ADD(cyc_serial, c0);
+#ifdef ARROW_PROF
+      if (lane == 0) {
+        u().cyc_kind[prof_kind] += c1 - c0;
+        u().cyc_kind[7] += clock_now() - c1;
+      }
+#endif
     }
     // end-of-run checks, engine.py:286-290
     const int completed = u().completed;
@@ -2219,6 +2321,10 @@ struct Sim {
       out->n_serial_steps = U.n_serial;
       out->n_parallel_steps = U.n_rounds + U.n_bursts;
       out->cycles = clock_now() - t_start;
+#if defined(ARROW_PROF) && defined(__CUDA_ARCH__)
+      if (sid < ARROW_PROF_MAX)
+        for (int q = 0; q < 16; q++) arrow_prof_cycles[sid * 16 + q] = U.cyc_kind[q];
+#endif
       {  // profiling: per-mille of loop cycles in serial steps (high word) and rounds (low word)
         const int64_t tot = U.cyc_serial + U.cyc_round + U.cyc_burst + 1;
         out->reserved = ((U.cyc_serial * 1000 / tot) << 32) | (U.cyc_round * 1000 / tot);

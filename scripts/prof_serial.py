@@ -1,0 +1,45 @@
+"""Serial-step cycle breakdown by event kind (needs a -DARROW_PROF build).
+
+    ARROW_SIM_LIB=/tmp/libprof.so python scripts/prof_serial.py
+"""
+import ctypes
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    import torch
+
+    from paper_2505_11916_b200 import engine, workloads as W
+    from paper_2505_11916_b200._backend import CudaEvaluator, load_library
+    from paper_2505_11916_b200._buffers import OutputSpec
+    from paper_2505_11916_b200._compile import compile_batch, dispatch_order
+
+    scen = W.c2(trace=W.c2_variant_trace(0))
+    ev = CudaEvaluator()
+    cb = compile_batch(scen, engine.STALL_EVENT_LIMIT)
+    hb = ev.execute(cb, OutputSpec(), dispatch_order(cb))
+    lib = load_library()
+    out = np.zeros(len(scen) * 16, dtype=np.int64)
+    rc = lib.arrow_sim_prof(out.ctypes.data_as(ctypes.c_void_p), len(scen))
+    assert rc == 0, rc
+    p = out.reshape(-1, 16)
+    names = ["-", "-", "prefill_c", "arrival", "tick", "loud_iter", "migration", "rescan", "burst_sel", "burst_run", "round_sel", "round_run", "chains", "merge", "-", "-"]
+    cyc = hb.summaries["cycles"]
+    top = np.argsort(-cyc)[:6]
+    for k in top:
+        tot = cyc[k]
+        parts = ", ".join(f"{names[q]} {100 * p[k, q] / tot:.1f}%" for q in range(16) if names[q] != "-")
+        print(f"scenario {k}: {tot / 1e6:.1f}M cycles: {parts}")
+    agg = p.sum(0) / cyc.sum()
+    print("all:", ", ".join(f"{names[q]} {100 * agg[q]:.1f}%" for q in range(16) if names[q] != "-"))
+
+
+if __name__ == "__main__":
+    main()
