@@ -16,9 +16,12 @@ namespace {
 
 constexpr int kWarpsPerBlock = 4;
 constexpr int kThreads = kWarpsPerBlock * 32;
+#ifndef ARROW_MIN_BLOCKS
+#define ARROW_MIN_BLOCKS 1
+#endif
 
 template <int IPL>
-__global__ void __launch_bounds__(kThreads) arrow_sim_kernel(const arrow_batch_t batch, char* workspace,
+__global__ void __launch_bounds__(kThreads, ARROW_MIN_BLOCKS) arrow_sim_kernel(const arrow_batch_t batch, char* workspace,
                                                              arrow::SlotLayout L, int* counter, int n_slots) {
   __shared__ arrow::WarpSmem smem[kWarpsPerBlock];
   __shared__ arrow_batch_t sb;

@@ -141,3 +141,40 @@ def test_sweep_on_device_traces_matches_host_traces():
     assert [r.token_times for r in r_dev.records] == [r.token_times for r in r_host.records]
     # rate sweep through the drop-in report API
     assert arrow.run_rate_sweep(ts[0], cfg, [5.0, 10.0]) == arrow.run_rate_sweep(hosts[0], cfg, [5.0, 10.0])
+
+
+def test_multi_seed_sweep_vs_oracle(monkeypatch):
+    """A multi-seed sweep the way the device generator is meant to be used:
+    24 seeds generated on the GPU, each evaluated in place under Arrow /
+    static PD / colocated at two rates; every summary field and the
+    decision-stream digest equal the CPU oracle run on the same traces."""
+    import paper_2505_11916_b200 as arrow
+    import scenarios as S
+    from paper_2505_11916_b200._buffers import OutputSpec
+    from paper_2505_11916_b200._compile import Scenario, compile_batch
+
+    monkeypatch.setattr(arrow.engine, "STALL_EVENT_LIMIT", 20000)  # read per call, like engine.py:283
+    base = SH.params_of(dict(SH.catalogue())["bursty"])
+    ts = arrow.gen_synthetic_batch([replace(base, duration_s=120.0, seed=9000 + s) for s in range(24)])
+    arrow_cfg = arrow.config_from_values(S.cfg(instances=8, kv_capacity_tokens=4400, a2=2e-8, a1=2e-5, a0=2e-3))
+    static_cfg = replace(arrow_cfg, scheduler=replace(arrow_cfg.scheduler, strategy=arrow.Strategy.MINIMAL_LOAD))
+    coloc = arrow.config_from_values(S.cfg(instances=8, init_prefill=8, init_decode=0, enable_flips=False,
+                                           kv_capacity_tokens=4400, a2=2e-8, a1=2e-5, a0=2e-3))
+    dev, host = [], []
+    hosts = [dt.to_host() for dt in ts]
+    for k, dt in enumerate(ts):
+        for cfg in (arrow_cfg, static_cfg, coloc):
+            for rate in (8.0, 20.0):
+                scale = arrow.native_rate(dt) / rate
+                dev.append(Scenario(dt, cfg, scale))
+                host.append(Scenario(hosts[k], cfg, scale))
+    got = arrow.evaluate_scenarios(dev)
+    exp = H.run_oracle(compile_batch(host, 20000), OutputSpec(), threads=0)
+    for s in range(len(dev)):
+        g, e = got.summaries[s], exp.summaries[s]
+        for f in ("status", "n_completed", "n_ok", "n_flips", "n_events", "n_iterations", "n_decisions", "n_ticks",
+                  "decision_hash"):
+            assert int(g[f]) == int(e[f]), (s, f, g[f], e[f])
+        for f in ("stall_time", "attainment", "p90_ttft", "p90_tpot", "mean_ttft", "mean_tpot", "goodput", "span"):
+            H.assert_same_f64([g[f]], [e[f]], f"scenario {s} {f}")
+    assert (got.summaries["status"] == _abi.OK).sum() > len(dev) // 2
