@@ -16,13 +16,16 @@ namespace {
 
 constexpr int kWarpsPerBlock = 4;
 constexpr int kThreads = kWarpsPerBlock * 32;
-#ifndef ARROW_MIN_BLOCKS
-#define ARROW_MIN_BLOCKS 1
-#endif
+// Two builds of the kernel: MINB = 1 lets the compiler use every register it
+// wants (shortest per-scenario chains: a sweep that fits in one wave of
+// resident warps finishes when its longest scenario does); MINB = 3 caps
+// registers at 168 so three blocks (12 warps) share an SM (throughput for
+// sweeps of many waves, where issue slots, not chain latency, are the bound).
+constexpr int kMinBlocksThroughput = 3;
 
-template <int IPL>
-__global__ void __launch_bounds__(kThreads, ARROW_MIN_BLOCKS) arrow_sim_kernel(const arrow_batch_t batch, char* workspace,
-                                                             arrow::SlotLayout L, int* counter, int n_slots) {
+template <int IPL, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) arrow_sim_kernel(const arrow_batch_t batch, char* workspace,
+                                                                   arrow::SlotLayout L, int* counter, int n_slots) {
   __shared__ arrow::WarpSmem smem[kWarpsPerBlock];
   __shared__ arrow_batch_t sb;
   if (threadIdx.x == 0) sb = batch;
@@ -53,23 +56,38 @@ arrow::SlotLayout layout_of(const arrow_batch_t* b) {
 
 int ipl_of(const arrow_batch_t* b) { return b->max_instances > 32 ? 2 : 1; }
 
-cudaError_t slots_for(const arrow_batch_t* b, int* slots) {
+template <int IPL, int MINB>
+cudaError_t capacity_of(int sms, long long* cap) {
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arrow_sim_kernel<IPL, MINB>, kThreads, 0);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  *cap = (long long)sms * per_sm * kWarpsPerBlock;
+  return cudaSuccess;
+}
+
+// Resident scenario slots and the kernel build: the latency build when the
+// whole batch fits in its single wave, the occupancy build otherwise.
+cudaError_t slots_for(const arrow_batch_t* b, int* slots, bool* throughput) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   int sms = 0;
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  if (ipl_of(b) == 2)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arrow_sim_kernel<2>, kThreads, 0);
-  else
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arrow_sim_kernel<1>, kThreads, 0);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) per_sm = 1;
-  long long cap = (long long)sms * per_sm * kWarpsPerBlock;
-  long long want = b->n_scenarios > 0 ? b->n_scenarios : 1;
+  long long lat = 0, thr = 0;
+  if (ipl_of(b) == 2) {
+    if ((e = capacity_of<2, 1>(sms, &lat)) != cudaSuccess) return e;
+    if ((e = capacity_of<2, kMinBlocksThroughput>(sms, &thr)) != cudaSuccess) return e;
+  } else {
+    if ((e = capacity_of<1, 1>(sms, &lat)) != cudaSuccess) return e;
+    if ((e = capacity_of<1, kMinBlocksThroughput>(sms, &thr)) != cudaSuccess) return e;
+  }
+  const long long want = b->n_scenarios > 0 ? b->n_scenarios : 1;
+  const bool tp = want > lat;
+  const long long cap = tp ? thr : lat;
   *slots = (int)(want < cap ? want : cap);
+  if (throughput) *throughput = tp;
   return cudaSuccess;
 }
 
@@ -79,13 +97,13 @@ extern "C" {
 
 int arrow_sim_abi_version(void) { return ARROW_SIM_ABI_VERSION; }
 
-int arrow_sim_slots(const arrow_batch_t* b, int* slots) { return (int)slots_for(b, slots); }
+int arrow_sim_slots(const arrow_batch_t* b, int* slots) { return (int)slots_for(b, slots, nullptr); }
 
 int arrow_sim_workspace_size(const arrow_batch_t* b, size_t* bytes) {
   if (!b || !bytes) return (int)cudaErrorInvalidValue;
   if (b->max_instances < 1 || b->max_instances > arrow::MAX_INST) return (int)cudaErrorInvalidValue;
   int slots = 0;
-  cudaError_t e = slots_for(b, &slots);
+  cudaError_t e = slots_for(b, &slots, nullptr);
   if (e != cudaSuccess) return (int)e;
   arrow::SlotLayout L = layout_of(b);
   *bytes = (size_t)slots * (size_t)L.bytes + 256;
@@ -100,7 +118,8 @@ int arrow_sim_run(const arrow_batch_t* b, void* workspace, size_t workspace_byte
   if (rc) return rc;
   if (!workspace || workspace_bytes < need) return (int)cudaErrorInvalidValue;
   int slots = 0;
-  cudaError_t e = slots_for(b, &slots);
+  bool tp = false;
+  cudaError_t e = slots_for(b, &slots, &tp);
   if (e != cudaSuccess) return (int)e;
   arrow::SlotLayout L = layout_of(b);
   char* ws = (char*)workspace;
@@ -109,10 +128,17 @@ int arrow_sim_run(const arrow_batch_t* b, void* workspace, size_t workspace_byte
   e = cudaMemsetAsync(counter, 0, sizeof(int), st);
   if (e != cudaSuccess) return (int)e;
   const int grid = (slots + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  if (ipl_of(b) == 2)
-    arrow_sim_kernel<2><<<grid, kThreads, 0, st>>>(*b, ws, L, counter, slots);
-  else
-    arrow_sim_kernel<1><<<grid, kThreads, 0, st>>>(*b, ws, L, counter, slots);
+  if (ipl_of(b) == 2) {
+    if (tp)
+      arrow_sim_kernel<2, kMinBlocksThroughput><<<grid, kThreads, 0, st>>>(*b, ws, L, counter, slots);
+    else
+      arrow_sim_kernel<2, 1><<<grid, kThreads, 0, st>>>(*b, ws, L, counter, slots);
+  } else {
+    if (tp)
+      arrow_sim_kernel<1, kMinBlocksThroughput><<<grid, kThreads, 0, st>>>(*b, ws, L, counter, slots);
+    else
+      arrow_sim_kernel<1, 1><<<grid, kThreads, 0, st>>>(*b, ws, L, counter, slots);
+  }
   return (int)cudaGetLastError();
 }
 

@@ -174,7 +174,6 @@ struct WarpSmem {
   int bhead[MAX_INST];           // merge cursor (tie fallback)
   int blast[MAX_INST];           // its last event pushed a successor
   uint32_t bseq[MAX_INST];       // sequence of its head / final pending push
-  uint64_t bfinal[MAX_INST];     // key of its final pushing event (~0: none)
   int btie;
 };
 
@@ -1851,31 +1850,6 @@ struct Sim {
     return lo;
   }
 
-  // Entries of the sorted a[0..n) below x, and whether x occurs.  Chains are
-  // short (a few events): independent loads four at a time beat the
-  // dependent shared-memory loads of a binary search; long lists search.
-  static AS_HD int count_below_u64(const uint64_t* a, int n, uint64_t x, bool& eq) {
-    if (n > 16) {
-      const int lb = lower_bound_u64(a, n, x);
-      eq = lb < n && a[lb] == x;
-      return lb;
-    }
-    int c = 0;
-    bool e = false;
-    int j = 0;
-    for (; j + 4 <= n; j += 4) {
-      const uint64_t v0 = a[j], v1 = a[j + 1], v2 = a[j + 2], v3 = a[j + 3];
-      c += (int)(v0 < x) + (int)(v1 < x) + (int)(v2 < x) + (int)(v3 < x);
-      e = e || v0 == x || v1 == x || v2 == x || v3 == x;
-    }
-    for (; j < n; j++) {
-      const uint64_t v = a[j];
-      c += (int)(v < x);
-      e = e || v == x;
-    }
-    eq = e;
-    return c;
-  }
 
   AS_HD void run_burst(const bool safe[IPL], const Head& hz, int per, Head& h) {
     // segments: participant rank (slot-major, then lane) x per
@@ -1914,54 +1888,34 @@ struct Sim {
     w.sync();
     PROF_MARK(12, pb0);
     PROF_CLOCK(pb1);
-    // Sequence numbers only order events with equal times, and the pushes
-    // inside a burst belong to events already executed: what the final
-    // pending push of each chain must carry is its order relative to the
-    // other chains' final pushes (by the time of the event that pushed it)
-    // and a value in [base, base + total pushes), above every earlier push
-    // and below every later one.  Rank among the finals gives exactly that;
-    // equal final times fall back to the sequential merge below, which
-    // reproduces the full (time, seq) order.
+    // The final pending push of each chain gets the global counter value it
+    // would have had: base + pushes (all chains) ordered before it.  Pushes
+    // inside the burst belong to events already executed, so their own
+    // numbers are never compared again.  Exact time ties with another
+    // chain's event fall back to a sequential merge.
     int before[IPL];
-    uint64_t xlast[IPL];  // key of each chain's final (pending-push) event
 #pragma unroll
-    for (int k = 0; k < IPL; k++) {
-      before[k] = 0;
-      xlast[k] = ~0ull;
-      if (st[k].id < 0) continue;
-      const int id = st[k].id;
-      if (safe[k] && lastp[k]) xlast[k] = sm->blist[sm->boff[id] + sm->bcount[id] - 1];
-      sm->bfinal[id] = xlast[k];
-    }
-    const int n_final = (int)w.add_u32((uint32_t)(
-        (IPL > 0 && safe[0] && lastp[0] ? 1 : 0) + (IPL > 1 && safe[IPL - 1] && lastp[IPL - 1] ? 1 : 0)));
-    w.sync();
-    bool tie_seen = false;
-    {
-      const int N = sc().n_instances;
+    for (int k = 0; k < IPL; k++) before[k] = sm->bcount[st[k].id >= 0 ? st[k].id : 0] - 1;
 #pragma unroll
-      for (int k = 0; k < IPL; k++) {
-        if (!(safe[k] && lastp[k])) continue;
-        const uint64_t x = xlast[k];
-        int r = 0;
-        bool eq = false;
-        int i = 0;
-        for (; i + 4 <= N; i += 4) {
-          const uint64_t v0 = sm->bfinal[i], v1 = sm->bfinal[i + 1], v2 = sm->bfinal[i + 2], v3 = sm->bfinal[i + 3];
-          r += (int)(v0 < x) + (int)(v1 < x) + (int)(v2 < x) + (int)(v3 < x);
-          eq = eq || (v0 == x && i != st[k].id) || (v1 == x && i + 1 != st[k].id) ||
-               (v2 == x && i + 2 != st[k].id) || (v3 == x && i + 3 != st[k].id);
+    for (int kk = 0; kk < IPL; kk++) {
+      uint32_t m = w.ballot(safe[kk]);
+      while (m) {
+        const int j = ffs32(m);
+        m &= m - 1;
+        const int other = w.shfl(st[kk].id, j);
+        const uint64_t* lst = sm->blist + sm->boff[other];
+        const int n_o = sm->bcount[other];
+        const int last_o = sm->blast[other];
+#pragma unroll
+        for (int k = 0; k < IPL; k++) {
+          if (!safe[k] || !lastp[k] || st[k].id == other) continue;
+          const uint64_t x = sm->blist[sm->boff[st[k].id] + sm->bcount[st[k].id] - 1];
+          const int lb = lower_bound_u64(lst, n_o, x);
+          if (lb < n_o && lst[lb] == x) sm->btie = 1;
+          before[k] += lb - ((lb == n_o && !last_o) ? 1 : 0);
         }
-        for (; i < N; i++) {
-          const uint64_t v = sm->bfinal[i];
-          r += (int)(v < x);
-          eq = eq || (v == x && i != st[k].id);
-        }
-        before[k] = r;
-        tie_seen = tie_seen || eq;
       }
     }
-    if (tie_seen) sm->btie = 1;
     const uint32_t packed = w.add_u32((uint32_t)events | ((uint32_t)completed << 16));
     const uint32_t total_push = w.add_u32((uint32_t)pushes);
     w.sync();
@@ -1969,7 +1923,7 @@ struct Sim {
     if (!tie) {
 #pragma unroll
       for (int k = 0; k < IPL; k++)
-        if (safe[k] && lastp[k]) st[k].iter_seq = base + total_push - (uint32_t)n_final + (uint32_t)before[k];
+        if (safe[k] && lastp[k]) st[k].iter_seq = base + (uint32_t)before[k];
     } else {
       // sequential merge of all chains in (time, seq) order; bseq[i] holds
       // the sequence of chain i's current head event
