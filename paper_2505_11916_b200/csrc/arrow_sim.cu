@@ -14,6 +14,9 @@
 
 namespace {
 
+#ifndef ARROW_LAT_WARPS
+#define ARROW_LAT_WARPS 2
+#endif
 constexpr int kWarpsPerBlock = 4;
 constexpr int kThreads = kWarpsPerBlock * 32;
 // Two builds of the kernel: MINB = 1 lets the compiler use every register it
@@ -22,16 +25,17 @@ constexpr int kThreads = kWarpsPerBlock * 32;
 // registers at 168 so three blocks (12 warps) share an SM (throughput for
 // sweeps of many waves, where issue slots, not chain latency, are the bound).
 constexpr int kMinBlocksThroughput = 3;
+constexpr int kLatWarps = ARROW_LAT_WARPS;  // warps per block of the latency build
 
-template <int IPL, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) arrow_sim_kernel(const arrow_batch_t batch, char* workspace,
+template <int IPL, int MINB, int WPB>
+__global__ void __launch_bounds__(WPB * 32, MINB) arrow_sim_kernel(const arrow_batch_t batch, char* workspace,
                                                                    arrow::SlotLayout L, int* counter, int n_slots) {
-  __shared__ arrow::WarpSmem smem[kWarpsPerBlock];
+  __shared__ arrow::WarpSmem smem[WPB];
   __shared__ arrow_batch_t sb;
   if (threadIdx.x == 0) sb = batch;
   __syncthreads();
   const int wid = threadIdx.x >> 5;
-  const int slot = blockIdx.x * kWarpsPerBlock + wid;
+  const int slot = blockIdx.x * WPB + wid;
   if (slot >= n_slots) return;
   arrow::Sim<DevWarp, IPL> sim;
   sim.sm = &smem[wid];
@@ -56,13 +60,14 @@ arrow::SlotLayout layout_of(const arrow_batch_t* b) {
 
 int ipl_of(const arrow_batch_t* b) { return b->max_instances > 32 ? 2 : 1; }
 
-template <int IPL, int MINB>
+template <int IPL, int MINB, int WPB>
 cudaError_t capacity_of(int sms, long long* cap) {
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arrow_sim_kernel<IPL, MINB>, kThreads, 0);
+  cudaError_t e =
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arrow_sim_kernel<IPL, MINB, WPB>, WPB * 32, 0);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  *cap = (long long)sms * per_sm * kWarpsPerBlock;
+  *cap = (long long)sms * per_sm * WPB;
   return cudaSuccess;
 }
 
@@ -77,11 +82,11 @@ cudaError_t slots_for(const arrow_batch_t* b, int* slots, bool* throughput) {
   if (e != cudaSuccess) return e;
   long long lat = 0, thr = 0;
   if (ipl_of(b) == 2) {
-    if ((e = capacity_of<2, 1>(sms, &lat)) != cudaSuccess) return e;
-    if ((e = capacity_of<2, kMinBlocksThroughput>(sms, &thr)) != cudaSuccess) return e;
+    if ((e = capacity_of<2, 1, kLatWarps>(sms, &lat)) != cudaSuccess) return e;
+    if ((e = capacity_of<2, kMinBlocksThroughput, kWarpsPerBlock>(sms, &thr)) != cudaSuccess) return e;
   } else {
-    if ((e = capacity_of<1, 1>(sms, &lat)) != cudaSuccess) return e;
-    if ((e = capacity_of<1, kMinBlocksThroughput>(sms, &thr)) != cudaSuccess) return e;
+    if ((e = capacity_of<1, 1, kLatWarps>(sms, &lat)) != cudaSuccess) return e;
+    if ((e = capacity_of<1, kMinBlocksThroughput, kWarpsPerBlock>(sms, &thr)) != cudaSuccess) return e;
   }
   const long long want = b->n_scenarios > 0 ? b->n_scenarios : 1;
   const bool tp = want > lat;
@@ -127,17 +132,18 @@ int arrow_sim_run(const arrow_batch_t* b, void* workspace, size_t workspace_byte
   cudaStream_t st = (cudaStream_t)stream;
   e = cudaMemsetAsync(counter, 0, sizeof(int), st);
   if (e != cudaSuccess) return (int)e;
-  const int grid = (slots + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int wpb = tp ? kWarpsPerBlock : kLatWarps;
+  const int grid = (slots + wpb - 1) / wpb;
   if (ipl_of(b) == 2) {
     if (tp)
-      arrow_sim_kernel<2, kMinBlocksThroughput><<<grid, kThreads, 0, st>>>(*b, ws, L, counter, slots);
+      arrow_sim_kernel<2, kMinBlocksThroughput, kWarpsPerBlock><<<grid, kThreads, 0, st>>>(*b, ws, L, counter, slots);
     else
-      arrow_sim_kernel<2, 1><<<grid, kThreads, 0, st>>>(*b, ws, L, counter, slots);
+      arrow_sim_kernel<2, 1, kLatWarps><<<grid, kLatWarps * 32, 0, st>>>(*b, ws, L, counter, slots);
   } else {
     if (tp)
-      arrow_sim_kernel<1, kMinBlocksThroughput><<<grid, kThreads, 0, st>>>(*b, ws, L, counter, slots);
+      arrow_sim_kernel<1, kMinBlocksThroughput, kWarpsPerBlock><<<grid, kThreads, 0, st>>>(*b, ws, L, counter, slots);
     else
-      arrow_sim_kernel<1, 1><<<grid, kThreads, 0, st>>>(*b, ws, L, counter, slots);
+      arrow_sim_kernel<1, 1, kLatWarps><<<grid, kLatWarps * 32, 0, st>>>(*b, ws, L, counter, slots);
   }
   return (int)cudaGetLastError();
 }
