@@ -28,7 +28,10 @@
 
 namespace {
 
-constexpr int kStatsThreads = 512;
+#ifndef ARROW_STATS_THREADS
+#define ARROW_STATS_THREADS 512
+#endif
+constexpr int kStatsThreads = ARROW_STATS_THREADS;
 constexpr int kPer = 4;                 // requests per lane per chunk (x2 buffers in flight)
 constexpr int kChunk = 32 * kPer;
 constexpr int kWarps = kStatsThreads / 32;
@@ -138,14 +141,14 @@ __device__ void warp_merge(Acc& a) {
   }
 }
 
-// hist[off + v - 1] += 1 for v in 1..kBins: one predicated red.shared on a
-// shared-window address (no generic-to-shared conversion per update).
+// hist[off + v - 1] += 1 for v in 1..kBins, else the spare word after both
+// histograms: one unconditional red.shared on a shared-window address (no
+// branch, no generic-to-shared conversion per update).
+constexpr int kHistWords = 2 * kBins + 32;  // + spare (keeps the ring 128 B aligned)
 __device__ __forceinline__ void hist_inc(uint32_t hist_sa, int32_t v, int off) {
-  const uint32_t a = hist_sa + 4u * (uint32_t)(off + v - 1);
-  asm volatile(
-      "{\n .reg .pred p;\n setp.lt.u32 p, %1, %2;\n @p red.shared.add.u32 [%0], 1;\n}" ::"r"(a),
-      "r"((uint32_t)(v - 1)), "r"((uint32_t)kBins)
-      : "memory");
+  const uint32_t b = (uint32_t)(v - 1);
+  const uint32_t idx = b < (uint32_t)kBins ? (uint32_t)off + b : (uint32_t)(2 * kBins);
+  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hist_sa + 4u * idx) : "memory");
 }
 
 __device__ __forceinline__ uint64_t warp_sum(uint64_t v) {
@@ -303,14 +306,17 @@ __device__ __forceinline__ void fold(const arrow_stats_args_t& A, Acc& acc, Run&
 
 // ---- TMA bulk-copy pipeline (cp.async.bulk + mbarrier), one ring per warp ----
 
-constexpr int kStages = 3;
+#ifndef ARROW_STATS_STAGES
+#define ARROW_STATS_STAGES 3
+#endif
+constexpr int kStages = ARROW_STATS_STAGES;
 struct Stage {  // one chunk of the SoA trace, as it sits in HBM
   double t[kChunk];
   int32_t x[kChunk], y[kChunk];
 };
 constexpr uint32_t kStageBytes = sizeof(Stage);
 static_assert(kStageBytes == 16 * kChunk, "stage = 16 B per request");
-constexpr size_t kHistBytes = 2 * kBins * sizeof(uint32_t);
+constexpr size_t kHistBytes = kHistWords * sizeof(uint32_t);
 constexpr size_t kSmemBytes = kHistBytes + (size_t)kWarps * kStages * kStageBytes;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -355,7 +361,7 @@ __global__ void __launch_bounds__(kStatsThreads, 1) arrow_stats_kernel(const arr
   uint32_t* hist = (uint32_t*)smem_raw;  // [2][kBins]
   __shared__ Acc red[kWarps];
   __shared__ uint64_t bars[kWarps][kStages];
-  for (int i = threadIdx.x; i < 2 * kBins; i += blockDim.x) hist[i] = 0;
+  for (int i = threadIdx.x; i < kHistWords; i += blockDim.x) hist[i] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
