@@ -322,10 +322,15 @@ def _finish(lib, torch, d, res, bucket_s, device, stream) -> TraceStats:
     m = _merge(res["partials"])
     lo = _floordiv_index(m["first"], bucket_s)
     hi = _floordiv_index(m["last"], bucket_s)
-    if m["oow"] or lo != res["lo"] or hi - lo + 1 != res["nb"]:
-        # the window hint disagreed with the data (cannot happen for exact hints)
+    for _ in range(3):
+        if not m["oow"] and lo == res["lo"] and hi - lo + 1 == res["nb"]:
+            break
+        # the window hint disagreed with the data (cannot happen for exact
+        # hints): rescan with the window of the scanned first / last arrival
         res = _run_scan(lib, torch, d, bucket_s, lo, hi - lo + 1, device, stream)
         m = _merge(res["partials"])
+        lo = _floordiv_index(m["first"], bucket_s)
+        hi = _floordiv_index(m["last"], bucket_s)
     assert m["n"] == d.n and not m["oow"], (m["n"], d.n, m["oow"])
     bk = res["buckets"]
     buckets = tuple(

@@ -110,3 +110,28 @@ def test_large_trace_radix_path():
         np.int64).tolist()
     assert abs(s.io_correlation - float(np.corrcoef(i.astype(float), o.astype(float))[0, 1])) < 1e-12
     assert ST.HIST_BINS == 16384
+
+
+def test_wrong_window_hint_is_rescanned():
+    """The scan trusts the host's window (first/last arrival) to track min /
+    max only in the edge buckets; a wrong window must be detected and
+    rescanned to the exact answer."""
+    import torch
+
+    import paper_2505_11916_b200 as arrow
+    from paper_2505_11916_b200 import stats as ST
+
+    c, (a, i, o) = next((c, arrs) for c, arrs in golden_cases() if c["name"] == "bursty_7p5")
+    trace = _trace(a, i, o)
+    b = c["bucket_s"]
+    dev = torch.device("cuda")
+    stream = torch.cuda.current_stream(dev)
+    lib = ST._lib()
+    for lo_shift, hi_shift in ((2, 0), (0, -3), (-1, 2), (5, -5)):
+        d = ST._Device(trace, dev)
+        lo = int(d.first_hint // b) + lo_shift
+        hi = int(d.last_hint // b) + hi_shift
+        res = ST._run_scan(lib, torch, d, b, lo, hi - lo + 1, dev, stream)
+        got = ST._finish(lib, torch, d, res, b, dev, stream)
+        assert_stats_equal(_as_dict(got), c, f"window shifted {lo_shift},{hi_shift}", corr_rtol=1e-12)
+    assert arrow.trace_stats(trace, b) == got
