@@ -174,6 +174,7 @@ struct WarpSmem {
   int bhead[MAX_INST];           // merge cursor (tie fallback)
   int blast[MAX_INST];           // its last event pushed a successor
   uint32_t bseq[MAX_INST];       // sequence of its head / final pending push
+  uint64_t bfinal[MAX_INST];     // key of its final pushing event (~0: none)
   int btie;
 };
 
@@ -1888,34 +1889,47 @@ struct Sim {
     w.sync();
     PROF_MARK(12, pb0);
     PROF_CLOCK(pb1);
-    // The final pending push of each chain gets the global counter value it
-    // would have had: base + pushes (all chains) ordered before it.  Pushes
-    // inside the burst belong to events already executed, so their own
-    // numbers are never compared again.  Exact time ties with another
-    // chain's event fall back to a sequential merge.
+    // Sequence numbers only order events with equal times, and the pushes
+    // inside a burst belong to events already executed: what the final
+    // pending push of each chain must carry is its order relative to the
+    // other chains' final pushes (by the time of the event that pushed it)
+    // and a value in [base, base + total pushes), above every earlier push
+    // and below every later one.  Rank among the finals gives exactly that;
+    // equal final times fall back to the sequential merge below, which
+    // reproduces the full (time, seq) order.
     int before[IPL];
+    uint64_t xlast[IPL];  // key of each chain's final (pending-push) event
 #pragma unroll
-    for (int k = 0; k < IPL; k++) before[k] = sm->bcount[st[k].id >= 0 ? st[k].id : 0] - 1;
+    for (int k = 0; k < IPL; k++) {
+      before[k] = 0;
+      xlast[k] = ~0ull;
+      if (st[k].id < 0) continue;
+      const int id = st[k].id;
+      if (safe[k] && lastp[k]) xlast[k] = sm->blist[sm->boff[id] + sm->bcount[id] - 1];
+      sm->bfinal[id] = xlast[k];
+    }
+    const int n_final = (int)w.add_u32((uint32_t)(
+        (IPL > 0 && safe[0] && lastp[0] ? 1 : 0) + (IPL > 1 && safe[IPL - 1] && lastp[IPL - 1] ? 1 : 0)));
+    w.sync();
+    bool tie_seen = false;
 #pragma unroll
     for (int kk = 0; kk < IPL; kk++) {
-      uint32_t m = w.ballot(safe[kk]);
+      // only the other finals matter: walk the warp's final-push mask
+      uint32_t m = w.ballot(safe[kk] && lastp[kk]);
       while (m) {
         const int j = ffs32(m);
         m &= m - 1;
-        const int other = w.shfl(st[kk].id, j);
-        const uint64_t* lst = sm->blist + sm->boff[other];
-        const int n_o = sm->bcount[other];
-        const int last_o = sm->blast[other];
+        const int other = j + WD * kk;  // instance i lives on lane i % WD, slot i / WD
+        const uint64_t v = sm->bfinal[other];
 #pragma unroll
         for (int k = 0; k < IPL; k++) {
-          if (!safe[k] || !lastp[k] || st[k].id == other) continue;
-          const uint64_t x = sm->blist[sm->boff[st[k].id] + sm->bcount[st[k].id] - 1];
-          const int lb = lower_bound_u64(lst, n_o, x);
-          if (lb < n_o && lst[lb] == x) sm->btie = 1;
-          before[k] += lb - ((lb == n_o && !last_o) ? 1 : 0);
+          if (!(safe[k] && lastp[k]) || st[k].id == other) continue;
+          before[k] += (int)(v < xlast[k]);
+          tie_seen = tie_seen || v == xlast[k];
         }
       }
     }
+    if (tie_seen) sm->btie = 1;
     const uint32_t packed = w.add_u32((uint32_t)events | ((uint32_t)completed << 16));
     const uint32_t total_push = w.add_u32((uint32_t)pushes);
     w.sync();
@@ -1923,7 +1937,7 @@ struct Sim {
     if (!tie) {
 #pragma unroll
       for (int k = 0; k < IPL; k++)
-        if (safe[k] && lastp[k]) st[k].iter_seq = base + (uint32_t)before[k];
+        if (safe[k] && lastp[k]) st[k].iter_seq = base + total_push - (uint32_t)n_final + (uint32_t)before[k];
     } else {
       // sequential merge of all chains in (time, seq) order; bseq[i] holds
       // the sequence of chain i's current head event
