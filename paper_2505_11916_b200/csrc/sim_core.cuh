@@ -853,9 +853,14 @@ struct Sim {
   // ---------------------------------------------------- scheduler ------
 
   AS_HD void compute_delays(double now) {
+    PROF_CLOCK(pd0);
 #pragma unroll
     for (int k = 0; k < IPL; k++)
       if (st[k].id >= 0) st[k].dly = delay(st[k], now);
+#ifdef ARROW_PROF
+    w.sync();
+#endif
+    PROF_MARK(14, pd0);
   }
 
   // _argmin over one pool (insertion order), key = delay
@@ -926,6 +931,14 @@ struct Sim {
 
   // decode_load_is_low, scheduler.py:136-147
   AS_HD bool decode_load_is_low(double now) {
+#ifdef ARROW_PROF
+    PROF_CLOCK(pl0);
+    const bool r = decode_load_is_low_(now);
+    PROF_MARK(15, pl0);
+    return r;
+  }
+  AS_HD bool decode_load_is_low_(double now) {
+#endif
     bool mine = false;
     uint32_t mn = ~0u;
 #pragma unroll
@@ -1625,60 +1638,76 @@ struct Sim {
   // Returns true and the horizon (events with key < hz are run) when some
   // chain-safe instance has an event before every other pending event;
   // `per` is the list segment each participant gets.
+  // The horizon only has to be a lower bound of the exact one (a burst that
+  // stops early is still exact: what it leaves runs in later steps), so the
+  // warp minima it is built from use the high word of the order key alone --
+  // one reduction each instead of a (high, low, sequence) argmin.
   AS_HD bool burst_select(const Head& h, Head& hz, bool safe[IPL], int& per) {
-    Head mine;
-    mine.code = -1;
-    mine.k = ~0ull;
-    mine.s = ~0u;
+    uint32_t ns_hi = ~0u;  // high key word of the earliest non-safe pending iteration
     bool any_safe = false;
 #pragma unroll
     for (int k = 0; k < IPL; k++) {
       const Inst& I = st[k];
       safe[k] = I.id >= 0 && chain_safe(I);
       any_safe = any_safe || safe[k];
-      if (I.id >= 0 && I.busy && !safe[k]) offer(mine, I.ck, EV_ITER, I.iter_seq, 2 * I.id + 1);
+      if (I.id >= 0 && I.busy && !safe[k] && (uint32_t)(I.ck >> 32) < ns_hi) ns_hi = (uint32_t)(I.ck >> 32);
     }
     if (!w.any(any_safe)) return false;
-    Head h2 = reduce_head(mine);
-    if (h.code >= 0 && (h2.code < 0 || h.k < h2.k || (h.k == h2.k && h.s < h2.s))) h2 = h;
-    uint64_t tmin = ~0ull;
+    ns_hi = w.min_u32(ns_hi);
+    // limit = min(serial head, non-safe events rounded down to their high word)
+    uint64_t lim_k = ~0ull;
+    uint32_t lim_s = ~0u;
+    bool lim = false;
+    if (ns_hi != ~0u) {
+      lim_k = (uint64_t)ns_hi << 32;
+      lim_s = 0;
+      lim = true;
+    }
+    if (h.code >= 0 && (!lim || h.k < lim_k)) {
+      lim_k = h.k;
+      lim_s = h.s;
+      lim = true;
+    }
+    uint32_t t_hi = ~0u;
     int n_mine = 0;
 #pragma unroll
     for (int k = 0; k < IPL; k++) {
       const Inst& I = st[k];
       const uint32_t k2 = ((uint32_t)EV_ITER << 28) | I.iter_seq;
-      safe[k] = safe[k] && (h2.code < 0 || I.ck < h2.k || (I.ck == h2.k && k2 < h2.s));
+      safe[k] = safe[k] && (!lim || I.ck < lim_k || (I.ck == lim_k && k2 < lim_s));
       if (safe[k]) {
         n_mine++;
-        if (I.ck < tmin) tmin = I.ck;
+        if ((uint32_t)(I.ck >> 32) < t_hi) t_hi = (uint32_t)(I.ck >> 32);
       }
     }
     const uint32_t n_part = w.add_u32((uint32_t)n_mine);
     if (n_part == 0) return false;
-    const uint32_t hi = w.min_u32((uint32_t)(tmin >> 32));
-    const uint32_t lo = w.min_u32((uint32_t)(tmin >> 32) == hi ? (uint32_t)tmin : ~0u);
+    t_hi = w.min_u32(t_hi);
     per = (int)(BURST_POOL / n_part);
     if (per > BURST_MAX) per = BURST_MAX;
     // at most `per` events per instance: decode-only iterations last >= b1 + b0
-    const double t0 = okey_inv(((uint64_t)hi << 32) | lo);
+    // (t0 <= the earliest participant's time)
+    const double t0 = okey_inv((uint64_t)t_hi << 32);
     uint64_t cap = tkey(t0 + (double)(per - 4) * (sc().b1 + sc().b0));
     {
-      uint64_t loud = ~0ull;
+      uint32_t l_hi = ~0u;
 #pragma unroll
       for (int k = 0; k < IPL; k++)
         if (safe[k]) {
-          const uint64_t b = chain_loud_bound(st[k]);
-          if (b < loud) loud = b;
+          const uint32_t bh = (uint32_t)(chain_loud_bound(st[k]) >> 32);
+          if (bh < l_hi) l_hi = bh;
         }
-      const uint32_t lhi = w.min_u32((uint32_t)(loud >> 32));
-      const uint32_t llo = w.min_u32((uint32_t)(loud >> 32) == lhi ? (uint32_t)loud : ~0u);
-      const uint64_t lb = ((uint64_t)lhi << 32) | llo;
+      l_hi = w.min_u32(l_hi);
+      const uint64_t lb = l_hi == ~0u ? ~0ull : ((uint64_t)l_hi << 32);
       if (lb < cap) cap = lb;
     }
-    hz = h2;
-    if (hz.code < 0 || cap < hz.k) {
+    if (!lim || cap < lim_k) {
       hz.k = cap;
       hz.s = 0;
+      hz.code = 0;
+    } else {
+      hz.k = lim_k;
+      hz.s = lim_s;
       hz.code = 0;
     }
     bool run = false;
