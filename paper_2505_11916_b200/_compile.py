@@ -19,6 +19,7 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass, field
 from functools import lru_cache
+from operator import attrgetter
 
 import numpy as np
 
@@ -34,6 +35,7 @@ from .cost_model import (
 )
 from .traces import trace_arrays
 
+_ID = attrgetter("id")
 KV_LIMIT = 1 << 30          # int32 KV arithmetic on the device
 MAX_INSTANCES = 64
 
@@ -68,11 +70,15 @@ def min_iteration(config: RunConfig) -> float:
     (b1 + b0) or a dedicated prefill of L <= chunk budget tokens
     (instance.py:207-212, 246-249), evaluated in the device's expression order."""
     inst = config.instance
-    dmin = inst.true_decode.b1 * 1.0 + inst.true_decode.b0
-    top = max(1, min(inst.chunk_budget, inst.kv_capacity_tokens, 1 << 20))
+    return _min_iteration(inst.true_decode.b1, inst.true_decode.b0, inst.true_prefill.a2, inst.true_prefill.a1,
+                          inst.true_prefill.a0, max(1, min(inst.chunk_budget, inst.kv_capacity_tokens, 1 << 20)))
+
+
+@lru_cache(maxsize=1024)
+def _min_iteration(b1: float, b0: float, a2: float, a1: float, a0: float, top: int) -> float:
+    dmin = b1 * 1.0 + b0
     L = np.arange(1, top + 1, dtype=np.float64)
-    p = inst.true_prefill
-    q = p.a2 * L * L + p.a1 * L + p.a0
+    q = a2 * L * L + a1 * L + a0
     return float(min(dmin, float(q.min())))
 
 
@@ -119,6 +125,19 @@ class TraceEntry:
     output_len: np.ndarray
     ids: np.ndarray
     offset: int = 0
+    _clean: bool | None = None
+    _max_kv: int = 0
+
+    def passes(self, scale: float, kv: int) -> bool:
+        """True when _validate_trace cannot raise for this scale and KV
+        capacity: a trace that is sorted with unique ids stays sorted under
+        any positive scale (rounding is monotone), leaving only the KV bound."""
+        if self._clean is None:
+            a = self.arrival
+            self._clean = bool(len(a) == 0 or ((a[1:] >= a[:-1]).all() and a[0] >= -1.0
+                                               and len(np.unique(self.ids)) == len(self.ids)))
+            self._max_kv = int((self.input_len.astype(np.int64) + self.output_len).max()) if len(a) else 0
+        return self._clean and scale > 0 and self._max_kv <= kv
 
 
 class DeviceTraceEntry:
@@ -191,7 +210,7 @@ class TraceTable:
             entry = trace
         else:
             arrival, inp, outp = trace_arrays(trace)
-            ids = np.fromiter((r.id for r in trace), dtype=np.int64, count=len(trace))
+            ids = np.fromiter(map(_ID, trace), dtype=np.int64, count=len(trace))
             entry = TraceEntry(arrival, inp, outp, ids)
         entry.offset = self.total
         self.total += len(entry.arrival)
@@ -291,6 +310,7 @@ def compile_batch(scenarios: list[Scenario], stall_limit: int, validate: bool = 
     ecap = 4
     rcap = 1
     validated: set = set()
+    templates: dict = {}
     for k, sc in enumerate(scenarios):
         t = table.add(sc.trace)
         entry = table.entries[t]
@@ -298,12 +318,20 @@ def compile_batch(scenarios: list[Scenario], stall_limit: int, validate: bool = 
         cfg = sc.config
         # reference order: predictor fit and token cap (in _Simulation.__init__)
         # raise before trace validation (in _Simulation.run)
-        recs[k] = scenario_record(cfg, entry.offset, n, sc.scale, stall_limit)
+        rkey = (id(cfg), entry.offset, n)
+        tmpl = templates.get(rkey)
+        if tmpl is None:  # one record per (config, trace); a sweep varies only the scale
+            tmpl = templates[rkey] = (cfg, scenario_record(cfg, entry.offset, n, 1.0, stall_limit))
+        recs[k] = tmpl[1]
+        recs[k]["arrival_scale"] = sc.scale
         if validate:
             vkey = (t, sc.scale, cfg.instance.kv_capacity_tokens)
             if isinstance(entry, DeviceTraceEntry) and entry.device.max_kv <= cfg.instance.kv_capacity_tokens:
                 # generated traces are sorted with ids 0..n-1 by construction
                 # (traces.py:166-175); only the KV bound can fail
+                validated.add(vkey)
+            if vkey not in validated and isinstance(entry, TraceEntry) and entry.passes(sc.scale,
+                                                                                  cfg.instance.kv_capacity_tokens):
                 validated.add(vkey)
             if vkey not in validated:
                 scaled = entry.arrival * sc.scale if sc.scale != 1.0 else entry.arrival

@@ -13,6 +13,7 @@ import csv
 import json
 import math
 from dataclasses import dataclass
+from operator import attrgetter
 from pathlib import Path
 
 import numpy as np
@@ -148,10 +149,13 @@ def bundled_ramp_trace() -> list[TraceRequest]:
 def trace_arrays(trace: list[TraceRequest]) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
     """Struct-of-arrays view of a trace: (arrival f64, input i32, output i32)."""
     n = len(trace)
-    arrival = np.fromiter((r.arrival for r in trace), dtype=np.float64, count=n)
-    inp = np.fromiter((r.input_len for r in trace), dtype=np.int32, count=n)
-    outp = np.fromiter((r.output_len for r in trace), dtype=np.int32, count=n)
+    arrival = np.fromiter(map(_ARRIVAL, trace), dtype=np.float64, count=n)
+    inp = np.fromiter(map(_INPUT, trace), dtype=np.int32, count=n)
+    outp = np.fromiter(map(_OUTPUT, trace), dtype=np.int32, count=n)
     return arrival, inp, outp
+
+
+_ARRIVAL, _INPUT, _OUTPUT = attrgetter("arrival"), attrgetter("input_len"), attrgetter("output_len")
 
 
 # -- canonical file formats (traces.py:23-102) -----------------------------
