@@ -226,7 +226,7 @@ typedef struct arrow_instdiag {
 
 typedef struct arrow_batch {
   int32_t n_scenarios;
-  int32_t flags;              /* reserved, 0 */
+  int32_t flags;              /* ARROW_SIM_FORCE_*: kernel build override (0 = by batch size) */
   /* sizing (max over scenarios), used for workspace layout */
   int32_t max_requests;
   int32_t max_instances;
@@ -254,6 +254,12 @@ typedef struct arrow_batch {
   arrow_instdiag_t* diag;
   double* token_times;        /* oracle only */
 } arrow_batch_t;
+
+/* arrow_batch_t.flags: the latency build (unbounded registers) is chosen when
+ * the batch fits in one wave of resident warps, the occupancy build otherwise;
+ * these force one (same results, different speed; used by the parity tests). */
+#define ARROW_SIM_FORCE_LATENCY 1
+#define ARROW_SIM_FORCE_THROUGHPUT 2
 
 /* ---- device library (libarrow_sim.so) ---- */
 

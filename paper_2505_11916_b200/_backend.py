@@ -161,9 +161,14 @@ class DeviceBatch:
 class CudaEvaluator:
     """Owns the device, the library handle and a reusable workspace."""
 
-    def __init__(self, device=None) -> None:
+    BUILDS = {None: 0, "latency": 1, "throughput": 2}  # ARROW_SIM_FORCE_* (include/arrow_sim.h)
+
+    def __init__(self, device=None, build: str | None = None) -> None:
+        """build: None picks the kernel build by batch size; "latency" /
+        "throughput" force one (identical results, different speed)."""
         import torch
 
+        self.flags = self.BUILDS[build]
         if not torch.cuda.is_available():
             raise EvaluatorUnavailable("no CUDA device: the Arrow evaluator runs only on the GPU (no CPU fallback)")
         self.torch = torch
@@ -201,6 +206,7 @@ class CudaEvaluator:
 
     def prepare(self, cb: CompiledBatch, spec: OutputSpec, order=None) -> DeviceBatch:
         hb = HostBuffers(cb, spec, order)
+        hb.flags = self.flags
         db = DeviceBatch(hb, self.device)
         db.upload()
         return db

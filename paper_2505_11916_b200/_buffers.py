@@ -101,6 +101,7 @@ class HostBuffers:
     def __init__(self, cb: CompiledBatch, spec: OutputSpec, order: np.ndarray | None = None) -> None:
         self.cb = cb
         self.spec = spec
+        self.flags = 0  # arrow_batch_t.flags (kernel build override, see arrow_sim.h)
         self.layout = lay = make_layout(cb, spec)
         self.order = None if order is None else np.ascontiguousarray(order, dtype=np.int32)
         self.summaries = np.zeros(cb.n, dtype=_abi.SUMMARY_DTYPE)
@@ -120,7 +121,7 @@ class HostBuffers:
     def fill_sizes(self, b: _abi.Batch) -> None:
         z = self.cb.sizes
         b.n_scenarios = self.cb.n
-        b.flags = 0
+        b.flags = self.flags
         b.max_requests = z["max_requests"]
         b.max_instances = z["max_instances"]
         b.queue_capacity = z["queue_capacity"]

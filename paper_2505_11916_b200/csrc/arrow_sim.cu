@@ -89,7 +89,9 @@ cudaError_t slots_for(const arrow_batch_t* b, int* slots, bool* throughput) {
     if ((e = capacity_of<1, kMinBlocksThroughput, kWarpsPerBlock>(sms, &thr)) != cudaSuccess) return e;
   }
   const long long want = b->n_scenarios > 0 ? b->n_scenarios : 1;
-  const bool tp = want > lat;
+  bool tp = want > lat;
+  if (b->flags & ARROW_SIM_FORCE_LATENCY) tp = false;
+  if (b->flags & ARROW_SIM_FORCE_THROUGHPUT) tp = true;
   const long long cap = tp ? thr : lat;
   *slots = (int)(want < cap ? want : cap);
   if (throughput) *throughput = tp;

@@ -134,3 +134,31 @@ def test_large_clusters_two_instances_per_lane(evaluator):
             H.assert_same_decisions(got.decisions_of(s), exp.decisions_of(s))
             sl = got.req_slice(s)
             H.assert_same_f64(got.req_last[sl], exp.req_last[sl], f"scenario {s} last")
+
+
+@pytest.mark.parametrize("build", ["latency", "throughput"])
+def test_both_kernel_builds_bit_exact(build):
+    """The latency build (unbounded registers) and the occupancy build
+    (3 blocks/SM) are the same source under different launch bounds; both,
+    forced regardless of batch size, reproduce the golden scenarios and the
+    oracle's random sweep (IPL 1 and 2)."""
+    from paper_2505_11916_b200._backend import CudaEvaluator
+
+    ev = CudaEvaluator(build=build)
+    items = _runnable()
+    by_limit: dict[int, list] = {}
+    for m, a in items:
+        by_limit.setdefault(m["stall_limit"], []).append((m, a))
+    for group in by_limit.values():
+        cb = H.compile_golden(group)
+        hb = ev.execute(cb, H.FULL)
+        for s, (m, a) in enumerate(group):
+            H.check_vs_golden(m, a, hb, s)
+    scs = _random_scenarios(7, 48)
+    cb = compile_batch(scs, 20000)
+    got = ev.execute(cb, OutputSpec(requests=True))
+    exp = H.run_oracle(cb, OutputSpec(requests=True), threads=0)
+    for s in range(cb.n):
+        for f in ("status", "n_completed", "n_ok", "n_flips", "n_events", "n_decisions", "decision_hash"):
+            assert int(got.summaries[s][f]) == int(exp.summaries[s][f]), (build, s, f)
+    np.testing.assert_array_equal(got.req_prefill, exp.req_prefill)
