@@ -26,12 +26,19 @@ $(LIB): $(SRCS) $(HDRS)
 oracle:
 	$(MAKE) -s -C oracle
 
-emu: build/libarrow_emu.so build/libnpgen_host.so
+emu: build/libarrow_emu.so build/libarrow_emu_wide.so build/libnpgen_host.so
 
 build/libarrow_emu.so: $(CSRC)/emu/emu.cpp $(HDRS)
 	@mkdir -p build
 	$(CXX_HOST) -std=c++20 -O2 -g -fPIC -shared -ffp-contract=off -fno-fast-math -pthread \
 		-Wall -Wno-unknown-pragmas -DARROW_EMU_TRACE -Iinclude -o $@ $(CSRC)/emu/emu.cpp
+
+# same emulator with delay intervals 2^40 times wider: most dispatches take the
+# exact-fold fallbacks (tests check both paths give the reference's decisions)
+build/libarrow_emu_wide.so: $(CSRC)/emu/emu.cpp $(HDRS)
+	@mkdir -p build
+	$(CXX_HOST) -std=c++20 -O2 -g -fPIC -shared -ffp-contract=off -fno-fast-math -pthread \
+		-Wall -Wno-unknown-pragmas -DARROW_DELAY_SLACK=0x1p-12 -Iinclude -o $@ $(CSRC)/emu/emu.cpp
 
 build/libnpgen_host.so: $(CSRC)/emu/npgen_host.cpp $(HDRS)
 	@mkdir -p build

@@ -89,8 +89,11 @@ def emission_capacity(config: RunConfig) -> int:
     dmin = min_iteration(config)
     if not (dmin > 0 and math.isfinite(dmin)):
         return 1 << 16
-    cap = math.floor(config.interval_window_s / dmin * (1 + 1e-9)) + 3
-    return int(min(max(cap, 4), 1 << 16))
+    window = math.floor(config.interval_window_s / dmin * (1 + 1e-9)) + 3
+    # Twice the window: a full ring is pruned (gallop + binary search from
+    # the head) once per ~window emissions instead of at every emission of
+    # a continuously busy instance.
+    return int(min(max(2 * window, 8), 1 << 17))
 
 
 def validate_trace(arrival_scaled: np.ndarray, ids: np.ndarray, inp: np.ndarray, outp: np.ndarray, kv: int) -> None:

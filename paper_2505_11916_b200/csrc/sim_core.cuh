@@ -58,6 +58,9 @@ namespace arrow {
 enum { EV_MIG = 0, EV_ITER = 1, EV_PREFILL = 2, EV_ARRIVAL = 3, EV_TICK = 4 };
 enum { P_PREFILL = 0, P_DECODE = 1, P_P2D = 2, P_D2P = 3 };
 static constexpr int MAX_INST = 64;
+#ifndef ARROW_DELAY_SLACK
+#define ARROW_DELAY_SLACK 0x1p-52  // per-term slack of the delay interval (tests widen it to force exact folds)
+#endif
 static constexpr uint32_t SEQ_LIMIT = 1u << 28;
 static constexpr int BURST_POOL = 512;  // chain-burst event keys per warp (shared memory)
 static constexpr int BURST_MAX = 64;    // events per instance per chain burst
@@ -207,7 +210,11 @@ struct Inst {
   double em_first, em_last;     // oldest / newest time in the emission ring (valid when em_c > 0)
   int cq;                       // cached: pending iteration is quiet
   uint64_t ck;                  // cached: order key of busy_until
-  double dly;                   // predicted_prefill_delay at the current event
+  double dly;                   // predicted_prefill_delay at the current event (exact iff dexact)
+  double dlo, dhi;              // interval certainly holding the exact predicted_prefill_delay
+  int dexact;                   // dly is the exact left fold
+  double ws_hi, ws_lo;          // waiting-prefill terms: double-double running sum ...
+  double ws_max;                // ... and the largest |term| since the queue was last empty
 };
 
 AS_HD uint64_t dbits(double x) {
@@ -448,6 +455,53 @@ struct Sim {
     }
     for (; j < c; j++) d += t[ring(h, j, cap)];
     return d;
+  }
+
+  // Double-double accumulate (hi, lo) += t (Knuth two-sum; no contraction).
+  AS_HD static void dd_add(double& hi, double& lo, double t) {
+    const double s = hi + t;
+    const double bb = s - hi;
+    const double e = (hi - (s - bb)) + (t - bb) + lo;
+    hi = s + e;
+    lo = e - (hi - s);
+  }
+
+  // The exact delay is a left fold of up to n = wp_c + 2 terms; instead of
+  // refolding a queue of up to hundreds of terms (a serially dependent chain
+  // of double additions) for every dispatch, bracket it: the fold differs from
+  // the real sum by at most (n - 1) u T (u = 2^-53, T = sum of |terms|), and
+  // x0 + rp + (exact running sum of the waiting terms) by at most a few u T,
+  // so [a - B, a + B] with B = (n + 8) 2^-52 T holds it.  Decisions that the
+  // interval settles (argmin winner strictly below every other candidate, a
+  // threshold test on the same side at both ends) are the reference's; the
+  // rest fold exactly (delay()).  With no waiting prefills the fold is
+  // x0 + rp itself and is exact.
+  AS_HD void delay_interval(Inst& I, double now) {
+    const arrow_scenario_t& s = sc();
+    double x0 = 0.0, rp = 0.0;
+    if (I.busy) {
+      const double x = I.busy_until - now;
+      x0 = (0.0 > x) ? 0.0 : x;
+    }
+    if (I.rp_rid >= 0) rp = quad(s.pred_a2, s.pred_a1, s.pred_a0, inl[I.rp_rid] - I.rp_done);
+    if (I.wp_c == 0) {
+      I.dly = I.dlo = I.dhi = (I.busy ? x0 : 0.0) + rp;  // the fold itself: 0.0 (+ x0) (+ rp)
+      I.dexact = 1;
+      return;
+    }
+    const double a = (x0 + rp) + (I.ws_hi + I.ws_lo);
+    const double T = x0 + fabs(rp) + (double)I.wp_c * I.ws_max;
+    const double B = (double)(I.wp_c + 10) * ARROW_DELAY_SLACK * T * (1.0 + 0x1p-30) + 0x1p-1000;
+    I.dly = a;
+    I.dlo = a - B;
+    I.dhi = a + B;
+    I.dexact = 0;
+  }
+
+  AS_HD void delay_exact(Inst& I, double now) {
+    if (I.dexact) return;
+    I.dly = I.dlo = I.dhi = delay(I, now);
+    I.dexact = 1;
   }
 
   // avg_token_interval, instance.py:323-329: over emissions with
@@ -761,8 +815,10 @@ struct Sim {
     }
     if (I.pb_k > 0) {
       const int* wp = wp_rid(I.id);
+      const double* wt = wp_term(I.id);
       for (int j = 0; j < I.pb_k; j++) {
         int rid = wp[ring(I.wp_h, j, L.qcap)];
+        dd_add(I.ws_hi, I.ws_lo, -wt[ring(I.wp_h, j, L.qcap)]);
         if (j < I.pb_k - 1 || I.pb_last_comp) {
           npf++;
           prefill_finished(I, rid, now, completed);
@@ -773,6 +829,7 @@ struct Sim {
       }
       I.wp_h = ring(I.wp_h, I.pb_k, L.qcap);
       I.wp_c -= I.pb_k;
+      if (I.wp_c == 0) I.ws_hi = I.ws_lo = I.ws_max = 0.0;
     }
     I.busy = 0;
     I.pb_ndec = I.pb_rp_chunk = I.pb_k = I.pb_last_chunk = I.pb_last_comp = I.pb_ded = 0;
@@ -856,7 +913,8 @@ struct Sim {
     PROF_CLOCK(pd0);
 #pragma unroll
     for (int k = 0; k < IPL; k++)
-      if (st[k].id >= 0) st[k].dly = delay(st[k], now);
+      if (st[k].id >= 0) delay_interval(st[k], now);
+    dnow = now;
 #ifdef ARROW_PROF
     w.sync();
 #endif
@@ -865,12 +923,72 @@ struct Sim {
 
   // _argmin over one pool (insertion order), key = delay
   AS_HD int argmin_delay_pool(int pool) {
+    return argmin_delay([&](const Inst& I) { return pool_of(I.id) == pool; },
+                        [&](const Inst& I) { return (uint32_t)pos_of(I.id); });
+  }
+
+  // Exact argmin of the predicted delay over the instances `sel` accepts,
+  // first minimum by `tie` (scheduler.py:89-99), from the delay intervals of
+  // compute_delays: only candidates whose interval reaches below every
+  // candidate's upper end can be the minimum; when more than one can, they
+  // fold exactly.
+  template <class Sel, class Tie>
+  AS_HD int argmin_delay(Sel sel, Tie tie_of) {
+    uint64_t mk = ~0ull;
+    bool cand[IPL];
+#pragma unroll
+    for (int k = 0; k < IPL; k++) {
+      cand[k] = st[k].id >= 0 && sel(st[k]);
+      if (cand[k]) {
+        const uint64_t x = okey(st[k].dhi);
+        if (x < mk) mk = x;
+      }
+    }
+    const uint32_t mhi = w.min_u32((uint32_t)(mk >> 32));
+    const uint32_t mlo = w.min_u32((uint32_t)(mk >> 32) == mhi ? (uint32_t)mk : ~0u);
+    mk = ((uint64_t)mhi << 32) | mlo;
+    int ncont = 0;
+    bool cont[IPL];
+#pragma unroll
+    for (int k = 0; k < IPL; k++) {
+      cont[k] = cand[k] && okey(st[k].dlo) <= mk;
+      ncont += popc32(w.ballot(cont[k]));
+    }
+    if (ncont > 1) {
+#pragma unroll
+      for (int k = 0; k < IPL; k++)
+        if (cont[k]) delay_exact(st[k], dnow);
+    }
     return argmin_inst([&](Inst& I, uint64_t& key, uint32_t& tie) {
-      if (pool_of(I.id) != pool) return false;
+      bool c = false;
+#pragma unroll
+      for (int k = 0; k < IPL; k++)
+        if (&I == &st[k]) c = cont[k];
+      if (!c) return false;
       key = okey(I.dly);
-      tie = (uint32_t)pos_of(I.id);
+      tie = tie_of(I);
       return true;
     });
+  }
+
+  // fl(delay + own) <= thr for instance id (monotone in the delay, so both
+  // interval ends on the same side decide it; otherwise fold exactly).
+  AS_HD bool delay_within(int id, double own, double thr) {
+    owner(id, [&](Inst& I) {
+      int r;
+      if (!I.dexact && I.dhi + own <= thr)
+        r = 1;
+      else if (!I.dexact && !(I.dlo + own <= thr))
+        r = 0;
+      else {
+        delay_exact(I, dnow);
+        r = I.dly + own <= thr ? 1 : 0;
+      }
+      u().tmp_i[0] = r;
+    });
+    const bool ok = u().tmp_i[0] != 0;
+    w.sync();
+    return ok;
   }
 
   AS_HD int argmin_tokens_pool(int pool) {
@@ -1010,20 +1128,14 @@ struct Sim {
     }
     const double thr = sc().ttft_thr;
     int t1 = argmin_delay_pool(P_PREFILL);
-    if (t1 >= 0) {
-      double d1 = bcast_d(t1, [](Inst& I) { return I.dly; });
-      if (d1 + own <= thr) {
-        log_dispatch(now, K, rid, t1, ARROW_BR_ALG1_T1);
-        return t1;
-      }
+    if (t1 >= 0 && delay_within(t1, own, thr)) {
+      log_dispatch(now, K, rid, t1, ARROW_BR_ALG1_T1);
+      return t1;
     }
     int t2 = argmin_delay_pool(P_D2P);
-    if (t2 >= 0) {
-      double d2 = bcast_d(t2, [](Inst& I) { return I.dly; });
-      if (d2 + own <= thr) {
-        log_dispatch(now, K, rid, t2, ARROW_BR_ALG1_T2);
-        return t2;
-      }
+    if (t2 >= 0 && delay_within(t2, own, thr)) {
+      log_dispatch(now, K, rid, t2, ARROW_BR_ALG1_T2);
+      return t2;
     }
     if (sc().enable_flips && decode_load_is_low(now)) {
       int t3 = try_move_d2p(now, ARROW_TRIG_ALG1);
@@ -1040,12 +1152,8 @@ struct Sim {
       log_dispatch(now, K, rid, t2, ARROW_BR_ALG1_FALLBACK);
       return t2;
     }
-    int chosen = argmin_inst([&](Inst& I, uint64_t& key, uint32_t& tie) {
-      if (!decode_role(I.id)) return false;
-      key = okey(I.dly);
-      tie = decode_role_tie(I.id);
-      return true;
-    });
+    int chosen = argmin_delay([&](const Inst& I) { return decode_role(I.id); },
+                              [&](const Inst& I) { return (uint32_t)decode_role_tie(I.id); });
     if (chosen < 0) {
       lane0([&] { set_status(ARROW_NO_INSTANCE); });
       return -1;
@@ -1142,6 +1250,8 @@ struct Sim {
       wp_rid(I.id)[slot] = rid;
       wp_term(I.id)[slot] = own;
       I.wp_c++;
+      dd_add(I.ws_hi, I.ws_lo, own);
+      if (fabs(own) > I.ws_max) I.ws_max = fabs(own);
       if (kick(I, now)) I.iter_seq = next_seq();
     });
   }
@@ -2343,6 +2453,7 @@ struct Sim {
   }
 
   int64_t t_start;
+  double dnow;  // event time of the last compute_delays (exact-fold fallbacks)
 
   AS_HD static int64_t clock_now() {
 #ifdef __CUDA_ARCH__

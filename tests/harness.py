@@ -50,15 +50,18 @@ def oracle_lib() -> ctypes.CDLL:
     return _libs["oracle"]
 
 
-def emu_lib() -> ctypes.CDLL:
-    if "emu" not in _libs:
-        path = ROOT / "build" / "libarrow_emu.so"
+def emu_lib(variant: str = "") -> ctypes.CDLL:
+    """variant "" is the kernel source as shipped; "wide" widens the delay
+    intervals so that most dispatch decisions take the exact-fold fallback."""
+    key = "emu" + variant
+    if key not in _libs:
+        path = ROOT / "build" / ("libarrow_emu_wide.so" if variant == "wide" else "libarrow_emu.so")
         _build("emu")
         lib = ctypes.CDLL(str(path))
         lib.arrow_emu_run.argtypes = [ctypes.c_void_p, ctypes.c_int]
         lib.arrow_emu_run.restype = ctypes.c_int
-        _libs["emu"] = lib
-    return _libs["emu"]
+        _libs[key] = lib
+    return _libs[key]
 
 
 def golden_index() -> list[dict]:
@@ -96,10 +99,10 @@ def run_oracle(cb, spec=FULL, threads=1, tokens=False) -> HostBuffers:
     return hb
 
 
-def run_emu(cb, spec=FULL, width=8) -> HostBuffers:
+def run_emu(cb, spec=FULL, width=8, variant: str = "") -> HostBuffers:
     hb = HostBuffers(cb, spec)
     b = hb.host_struct()
-    rc = emu_lib().arrow_emu_run(ctypes.addressof(b), width)
+    rc = emu_lib(variant).arrow_emu_run(ctypes.addressof(b), width)
     assert rc == 0, rc
     return hb
 

@@ -71,3 +71,18 @@ def test_emulated_kernel_matches_oracle_on_c2_points(index):
     if int(e["status"]) == 0:       # a stalled run raises; its partial records are never observed
         H.assert_same_f64(got.req_last, exp.req_last, "last")
         H.assert_same_decisions(got.decisions_of(0), exp.decisions_of(0))
+
+
+WIDE = [m for m in SMALL if m["name"].startswith(("fuzz_", "overload", "c1_", "small_", "migration", "tight"))]
+
+
+@pytest.mark.parametrize("meta", WIDE, ids=[m["name"] for m in WIDE])
+def test_exact_fold_fallbacks_match_reference(meta):
+    """Dispatches decide from delay intervals and fold exactly only when the
+    interval cannot settle them; with intervals 2^40 times wider (most
+    decisions then take the exact fallbacks) the kernel source must still
+    reproduce the reference bit for bit."""
+    arrays = H.golden_arrays(meta)
+    cb = H.compile_golden([(meta, arrays)])
+    hb = H.run_emu(cb, width=8, variant="wide")
+    H.check_vs_golden(meta, arrays, hb)
