@@ -98,7 +98,6 @@ typedef struct arrow_stats_partial {  /* one per block; merged on the host */
   uint64_t sxx_lo, sxx_hi;    /* 128-bit sums of x*x, y*y, x*y */
   uint64_t syy_lo, syy_hi;
   uint64_t sxy_lo, sxy_hi;
-  int32_t min_x, max_x, min_y, max_y;
   int64_t out_of_window;      /* requests whose bucket fell outside [bucket_lo, bucket_lo + n_buckets) */
 } arrow_stats_partial_t;
 

@@ -89,15 +89,12 @@ struct Acc {
   double tmin, tmax;
   int64_t count, sx, sy, oow;
   U128 sxx, syy, sxy;
-  int32_t mnx, mxx, mny, mxy;
 
   __device__ void init() {
     tmin = INFINITY;
     tmax = -INFINITY;
     count = sx = sy = oow = 0;
     sxx = syy = sxy = U128{0, 0};
-    mnx = mny = INT32_MAX;
-    mxx = mxy = INT32_MIN;
   }
   __device__ void merge(const Acc& o) {
     tmin = fmin(tmin, o.tmin);
@@ -109,10 +106,6 @@ struct Acc {
     sxx.add(o.sxx);
     syy.add(o.syy);
     sxy.add(o.sxy);
-    mnx = min(mnx, o.mnx);
-    mxx = max(mxx, o.mxx);
-    mny = min(mny, o.mny);
-    mxy = max(mxy, o.mxy);
   }
 };
 
@@ -133,10 +126,6 @@ __device__ void warp_merge(Acc& a) {
     o.sxx = U128{shfl_down(a.sxx.lo, d), shfl_down(a.sxx.hi, d)};
     o.syy = U128{shfl_down(a.syy.lo, d), shfl_down(a.syy.hi, d)};
     o.sxy = U128{shfl_down(a.sxy.lo, d), shfl_down(a.sxy.hi, d)};
-    o.mnx = shfl_down(a.mnx, d);
-    o.mxx = shfl_down(a.mxx, d);
-    o.mny = shfl_down(a.mny, d);
-    o.mxy = shfl_down(a.mxy, d);
     a.merge(o);
   }
 }
@@ -264,10 +253,6 @@ __device__ __forceinline__ void fold_chunk(const arrow_stats_args_t& A, Acc& acc
     if (v) {
       acc.tmin = t < acc.tmin ? t : acc.tmin;  // arrivals are never NaN
       acc.tmax = t > acc.tmax ? t : acc.tmax;
-      acc.mnx = min(acc.mnx, x);
-      acc.mxx = max(acc.mxx, x);
-      acc.mny = min(acc.mny, y);
-      acc.mxy = max(acc.mxy, y);
       // predicated shared-memory reductions on precomputed shared-window
       // addresses (lengths outside 1..kBins are counted on the host as
       // n - sum(bins))
@@ -460,10 +445,6 @@ __global__ void __launch_bounds__(kStatsThreads, 1) arrow_stats_kernel(const arr
     p.syy_hi = a.syy.hi;
     p.sxy_lo = a.sxy.lo;
     p.sxy_hi = a.sxy.hi;
-    p.min_x = a.mnx;
-    p.max_x = a.mxx;
-    p.min_y = a.mny;
-    p.max_y = a.mxy;
     p.out_of_window = a.oow;
     A.partials[blockIdx.x] = p;
   }
@@ -543,10 +524,6 @@ int arrow_stats_layout(int64_t* out, int cap) {
   OFF(arrow_stats_partial_t, syy_hi);
   OFF(arrow_stats_partial_t, sxy_lo);
   OFF(arrow_stats_partial_t, sxy_hi);
-  OFF(arrow_stats_partial_t, min_x);
-  OFF(arrow_stats_partial_t, max_x);
-  OFF(arrow_stats_partial_t, min_y);
-  OFF(arrow_stats_partial_t, max_y);
   OFF(arrow_stats_partial_t, out_of_window);
   OFF(arrow_stats_args_t, arrival);
   OFF(arrow_stats_args_t, input_len);

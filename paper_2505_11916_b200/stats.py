@@ -48,10 +48,6 @@ PARTIAL_DTYPE = np.dtype(
         ("syy_hi", np.uint64),
         ("sxy_lo", np.uint64),
         ("sxy_hi", np.uint64),
-        ("min_x", np.int32),
-        ("max_x", np.int32),
-        ("min_y", np.int32),
-        ("max_y", np.int32),
         ("out_of_window", np.int64),
     ],
     align=True,
@@ -192,9 +188,9 @@ class _Device:
             self.h2d = a.nbytes + i.nbytes + o.nbytes
 
 
-def _order_stats(lib, torch, values_dev, hist: np.ndarray, over: int, vmax: int, n: int, ranks, device, stream):
+def _order_stats(lib, torch, values_dev, hist: np.ndarray, over: int, n: int, ranks, device, stream):
     """k-th smallest lengths for every k in ranks: exact bins 1..16384, then a
-    two-level device radix select over the values above."""
+    two-level device radix select over the values above (up to 2^31 - 1)."""
     cum = np.cumsum(hist.astype(np.int64))
     in_bins = int(cum[-1])
     assert in_bins + over == n
@@ -207,7 +203,7 @@ def _order_stats(lib, torch, values_dev, hist: np.ndarray, over: int, vmax: int,
             need_high.append(k)
     if not need_high:
         return out
-    lo, hi = HIST_BINS + 1, vmax + 1
+    lo, hi = HIST_BINS + 1, 1 << 31
     shift = max(0, (hi - lo - 1).bit_length() - 20)
     nb = ((hi - lo - 1) >> shift) + 1
     bins = torch.empty(nb, dtype=torch.int32, device=device)
@@ -296,10 +292,6 @@ def _merge(p: np.ndarray) -> dict:
         sxx=sum(_u128(r["sxx_lo"], r["sxx_hi"]) for r in live),
         syy=sum(_u128(r["syy_lo"], r["syy_hi"]) for r in live),
         sxy=sum(_u128(r["sxy_lo"], r["sxy_hi"]) for r in live),
-        min_x=int(live["min_x"].min()),
-        max_x=int(live["max_x"].max()),
-        min_y=int(live["min_y"].min()),
-        max_y=int(live["max_y"].max()),
         oow=int(live["out_of_window"].sum()),
     )
 
@@ -337,22 +329,22 @@ def _finish(lib, torch, d, res, bucket_s, device, stream) -> TraceStats:
         BucketStats(lo + j, int(bk[0, j]), int(bk[1, j]), int(bk[2, j])) for j in range(hi - lo + 1)
     )
     n = m["n"]
-    if n >= 2 and m["min_x"] != m["max_x"] and m["min_y"] != m["max_y"]:
-        corr = pearson_from_moments(n, m["sx"], m["sy"], m["sxx"], m["syy"], m["sxy"])
-    else:
-        corr = 0.0
     duration = m["last"] - m["first"]
-    ranks = set()
+    ranks = {0, n - 1}  # min / max: the std > 0 tests of traces.py:238
     for p in (50, 90, 99):
         v = (n - 1) * np.true_divide(p, 100)
         f = int(np.floor(v))
         ranks.update(k for k in (f, f + 1) if 0 <= k < n)
-    ranks.add(n - 1)
     # lengths outside the exact bins: n - sum(bins)
     over_x = n - int(res["hist"][0].astype(np.int64).sum())
     over_y = n - int(res["hist"][1].astype(np.int64).sum())
-    osx = _order_stats(lib, torch, d.input_len, res["hist"][0], over_x, m["max_x"], n, sorted(ranks), device, stream)
-    osy = _order_stats(lib, torch, d.output_len, res["hist"][1], over_y, m["max_y"], n, sorted(ranks), device, stream)
+    osx = _order_stats(lib, torch, d.input_len, res["hist"][0], over_x, n, sorted(ranks), device, stream)
+    osy = _order_stats(lib, torch, d.output_len, res["hist"][1], over_y, n, sorted(ranks), device, stream)
+    # inputs.std() > 0 and outputs.std() > 0 <=> neither array is constant
+    if n >= 2 and osx[0] != osx[n - 1] and osy[0] != osy[n - 1]:
+        corr = pearson_from_moments(n, m["sx"], m["sy"], m["sxx"], m["syy"], m["sxy"])
+    else:
+        corr = 0.0
     return TraceStats(
         num_requests=n,
         duration_s=duration,

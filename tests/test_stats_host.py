@@ -88,7 +88,6 @@ def _partials_of(a, i, o, cuts) -> np.ndarray:
             for f, val in (("sxx", sum(v * v for v in x)), ("syy", sum(v * v for v in y)),
                            ("sxy", sum(u * v for u, v in zip(x, y)))):
                 p[f + "_lo"], p[f + "_hi"] = val & (2**64 - 1), val >> 64
-            p["min_x"], p["max_x"], p["min_y"], p["max_y"] = min(x), max(x), min(y), max(y)
         else:
             p["min_arrival"] = p["max_arrival"] = np.nan
         rows.append(p)
