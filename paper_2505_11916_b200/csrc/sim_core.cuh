@@ -1851,6 +1851,59 @@ struct Sim {
     last_pushed = 0;
     for (;;) {
       const int cur = I.it - 1;
+      // Steady stretch: no decode finishes before iteration min_f, no decode
+      // is waiting, so every completion up to there applies the same batch
+      // of R decodes and starts the next one (instance.py:187-191, 254-288):
+      // only the emission, the event key and t += b1*R + b0 (the very
+      // expression the general path evaluates) change per event; the
+      // counters advance in bulk afterwards.
+      if (!ilog && I.wd_c == 0 && I.min_f > cur && I.pb_ndec == I.R && I.R > 0 && I.R <= dcap) {
+        const int R = I.R;
+        const double dur = b1 * (double)R + b0;
+        int room = (int)L.ecap - I.em_c;
+        int kmax = I.min_f - cur;  // events cur, cur+1, ..., min_f - 1
+        if (kmax > room) kmax = room;
+        if (kmax > limit - c) kmax = limit - c;
+        if (kmax >= 2) {
+          int wpos = ring(I.em_h, I.em_c, L.ecap);
+          const int ecap = (int)L.ecap;
+          const double t_first = t;
+          int k = 0;
+          bool stop = false;
+          double t_emit = t;
+          while (k < kmax) {
+            e[wpos] = t;             // the event at t: emission (cur + k)
+            wpos = wpos + 1 == ecap ? 0 : wpos + 1;
+            t_emit = t;
+            bk[c++] = key;
+            k++;
+            t = t + dur;             // the iteration it starts
+            key = tkey(t);
+            if (key >= hz_k) {
+              stop = true;
+              break;
+            }
+          }
+          I.kv_used += R * k;
+          I.committed -= R * k;
+          I.rtok += R * k;
+          if (I.em_c == 0) I.em_first = t_first;
+          I.em_c += k;
+          I.em_last = t_emit;
+          I.it += k;
+          I.busy_until = t;
+          I.ck = key;
+          if (stop) {
+            last_pushed = 1;
+            return c;
+          }
+          if (c >= limit) {  // the horizon bounds the count; never taken
+            set_status(ARROW_INTERNAL);
+            return c;
+          }
+          continue;
+        }
+      }
       if (ilog) {
         if (cur < ilog_cap)
           ilog[cur] = t;

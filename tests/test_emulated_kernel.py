@@ -86,3 +86,17 @@ def test_exact_fold_fallbacks_match_reference(meta):
     cb = H.compile_golden([(meta, arrays)])
     hb = H.run_emu(cb, width=8, variant="wide")
     H.check_vs_golden(meta, arrays, hb)
+
+
+NO_ITERLOG = H.OutputSpec(requests=True, decisions=True, snapshots=True, diag=True)
+
+
+@pytest.mark.parametrize("meta", SMALL, ids=[m["name"] for m in SMALL])
+def test_emulated_kernel_without_iteration_log(meta):
+    """Without the per-iteration log output (the sweep configuration), chain
+    bursts take their steady-stretch fast path; decisions, token times,
+    summaries and snapshots must not change."""
+    arrays = H.golden_arrays(meta)
+    cb = H.compile_golden([(meta, arrays)])
+    hb = H.run_emu(cb, NO_ITERLOG, width=8)
+    H.check_vs_golden(meta, arrays, hb)
