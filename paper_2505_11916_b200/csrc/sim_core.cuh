@@ -947,14 +947,18 @@ struct Sim {
     const uint32_t mhi = w.min_u32((uint32_t)(mk >> 32));
     const uint32_t mlo = w.min_u32((uint32_t)(mk >> 32) == mhi ? (uint32_t)mk : ~0u);
     mk = ((uint64_t)mhi << 32) | mlo;
-    int ncont = 0;
+    int ncont = 0, single = -1;
     bool cont[IPL];
 #pragma unroll
     for (int k = 0; k < IPL; k++) {
       cont[k] = cand[k] && okey(st[k].dlo) <= mk;
-      ncont += popc32(w.ballot(cont[k]));
+      const uint32_t m = w.ballot(cont[k]);
+      ncont += popc32(m);
+      if (m) single = ffs32(m) + WD * k;  // instance i lives on lane i % WD, slot i / WD
     }
-    if (ncont > 1) {
+    if (ncont == 0) return -1;
+    if (ncont == 1) return single;  // the only candidate whose interval reaches the minimum
+    {
 #pragma unroll
       for (int k = 0; k < IPL; k++)
         if (cont[k]) delay_exact(st[k], dnow);
