@@ -118,6 +118,20 @@ def peaks() -> dict:
     return {"hbm_gbs": 6650.0, "source": "fallback"}
 
 
+def ncu_metric(workload: str, name: str):
+    """One metric of the committed `ncu --set full` capture of this bench's
+    kernel (profiles/<workload>_kernel_ncu_raw.csv), or None."""
+    import csv
+
+    path = ROOT / "profiles" / f"{workload}_kernel_ncu_raw.csv"
+    if not path.exists():
+        return None
+    rows = list(csv.reader(path.open()))
+    if name not in rows[0]:
+        return None
+    return float(rows[2][rows[0].index(name)])
+
+
 def ncu_traffic(workload: str):
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
     from the committed `ncu --set full` capture of this bench's kernel
@@ -329,6 +343,11 @@ def run_ours(args, rank: int, world: int) -> None:
         "traffic_source": f"profiles/{args.workload}_kernel_ncu_raw.csv (ncu --set full, one launch)",
         "peak_source": pk["source"],
         "note": "latency-bound serial event chains; algorithmic bytes = 40 B/request + 256 B/scenario",
+        # SM issue-slot utilisation of the same capture: the bound that applies
+        # (one warp per scheduler issuing a dependent chain)
+        "issue_slot_util": (lambda v: None if v is None else v / 100.0)(
+            ncu_metric(args.workload, "smsp__issue_active.avg.pct_of_peak_sustained_active")),
+        "cycles_per_issue": ncu_metric(args.workload, "smsp__average_warp_latency_per_inst_issued.ratio"),
     }
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
