@@ -1606,30 +1606,38 @@ struct Sim {
     return reduce_head(mine);
   }
 
-  // Quiet events before the head whose times are <= T = min(t_i + dl_i):
-  // one lane-parallel round.  Returns false when none qualifies.
-  AS_HD bool round_select(const Head& h, bool part[IPL]) {
+  // Quiet iterations pending before the serial head.  None means the head
+  // is the next event: no round and no burst (whose participants are quiet
+  // iterations before the head) can run, so the serial step follows at once.
+  AS_HD bool round_candidates(const Head& h, bool cand[IPL]) {
     bool any_cand = false;
-    uint64_t lim = ~0ull;
-    bool cand[IPL];
 #pragma unroll
     for (int k = 0; k < IPL; k++) {
       const Inst& I = st[k];
       const uint32_t k2 = ((uint32_t)EV_ITER << 28) | I.iter_seq;
       cand[k] = I.id >= 0 && I.busy && I.cq && (h.code < 0 || I.ck < h.k || (I.ck == h.k && k2 < h.s));
+      any_cand = any_cand || cand[k];
+    }
+    return w.any(any_cand);
+  }
+
+  // The candidates whose times are <= T = min(t_i + dl_i): one lane-parallel
+  // round.
+  AS_HD void round_select(const bool cand[IPL], bool part[IPL]) {
+    uint64_t lim = ~0ull;
+#pragma unroll
+    for (int k = 0; k < IPL; k++) {
+      const Inst& I = st[k];
       if (cand[k]) {
-        any_cand = true;
         const uint64_t x = tkey(I.busy_until + next_duration_bound(I));
         if (x < lim) lim = x;
       }
     }
-    if (!w.any(any_cand)) return false;
     const uint32_t hi = w.min_u32((uint32_t)(lim >> 32));
     const uint32_t lo = w.min_u32((uint32_t)(lim >> 32) == hi ? (uint32_t)lim : ~0u);
     const uint64_t cut = ((uint64_t)hi << 32) | lo;
 #pragma unroll
     for (int k = 0; k < IPL; k++) part[k] = cand[k] && st[k].ck <= cut;
-    return true;
   }
 
   // One parallel round of quiet iteration completions; folds any loud
@@ -2215,25 +2223,26 @@ struct Sim {
     Head h = full_scan();
     for (;;) {
       bool part[IPL];
+      bool cand[IPL];
       Head hz;
       int per = 0;
       PROF_CLOCK(c0);
-      const bool bsel = burst_select(h, hz, part, per);
-      PROF_MARK(8, c0);
-      if (bsel) {
-        PROF_CLOCK(cb);
-        run_burst(part, hz, per, h);
-        PROF_MARK(9, cb);
-        PROF_ADD(cyc_burst, c0);
-        const int status = u().status;
-        w.sync();
-        if (status != ARROW_OK) return;
-        continue;
-      }
-      PROF_CLOCK(cr);
-      const bool rsel = round_select(h, part);
-      PROF_MARK(10, cr);
-      if (rsel) {
+      if (round_candidates(h, cand)) {
+        const bool bsel = burst_select(h, hz, part, per);
+        PROF_MARK(8, c0);
+        if (bsel) {
+          PROF_CLOCK(cb);
+          run_burst(part, hz, per, h);
+          PROF_MARK(9, cb);
+          PROF_ADD(cyc_burst, c0);
+          const int status = u().status;
+          w.sync();
+          if (status != ARROW_OK) return;
+          continue;
+        }
+        PROF_CLOCK(cr);
+        round_select(cand, part);
+        PROF_MARK(10, cr);
         PROF_CLOCK(cx);
         run_round(part, h);
         PROF_MARK(11, cx);
@@ -2243,6 +2252,7 @@ struct Sim {
         if (status != ARROW_OK) return;
         continue;
       }
+      PROF_MARK(8, c0);
       if (h.code < 0) break;
       const int ev = h.code;
       double now = okey_inv(h.k);
