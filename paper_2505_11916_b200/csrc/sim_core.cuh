@@ -230,13 +230,12 @@ AS_HD uint64_t okey(double x) {
   return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
 
-// Order key of an event time: event times are never -0.0 (arrivals are
-// canonicalised on the host; every other time is t + positive duration), so
-// no canonicalising add is needed.
-AS_HD uint64_t tkey(double t) {
-  const uint64_t u = dbits(t);
-  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
-}
+// Order key of an event time.  Event times are >= +0.0 (arrivals are
+// validated >= 0 and canonicalised on the host, core.py:47-48; every other
+// time is t + a positive duration; the burst caps below are t + a positive
+// span), so the key is the bit pattern with the sign bit set: one OR instead
+// of okey's sign select and canonicalising add.
+AS_HD uint64_t tkey(double t) { return dbits(t) | 0x8000000000000000ull; }
 
 AS_HD double okey_inv(uint64_t k) {
   uint64_t u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
@@ -371,15 +370,19 @@ struct Sim {
   // ------------------------------------------------------ warp argmin --
 
   AS_HD int warp_argmin(uint64_t key, uint32_t tie, bool valid) {
-    if (w.ballot(valid) == 0) return -1;
-    uint64_t k = valid ? key : ~0ull;
-    uint32_t t = valid ? tie : ~0u;
-    uint32_t hi = w.min_u32((uint32_t)(k >> 32));
-    bool m = valid && (uint32_t)(k >> 32) == hi;
-    uint32_t lo = w.min_u32(m ? (uint32_t)k : ~0u);
-    m = m && (uint32_t)k == lo;
-    uint32_t tt = w.min_u32(m ? t : ~0u);
-    m = m && t == tt;
+    // each stage stops as soon as a single lane is left
+    uint32_t b = w.ballot(valid);
+    if ((b & (b - 1)) == 0) return b ? ffs32(b) : -1;
+    const uint32_t hi = w.min_u32(valid ? (uint32_t)(key >> 32) : ~0u);
+    bool m = valid && (uint32_t)(key >> 32) == hi;
+    b = w.ballot(m);
+    if ((b & (b - 1)) == 0) return ffs32(b);
+    const uint32_t lo = w.min_u32(m ? (uint32_t)key : ~0u);
+    m = m && (uint32_t)key == lo;
+    b = w.ballot(m);
+    if ((b & (b - 1)) == 0) return ffs32(b);
+    const uint32_t tt = w.min_u32(m ? tie : ~0u);
+    m = m && tie == tt;
     return ffs32(w.ballot(m));
   }
 
