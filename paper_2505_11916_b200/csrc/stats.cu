@@ -32,7 +32,10 @@ namespace {
 #define ARROW_STATS_THREADS 512
 #endif
 constexpr int kStatsThreads = ARROW_STATS_THREADS;
-constexpr int kPer = 4;                 // requests per lane per chunk (x2 buffers in flight)
+#ifndef ARROW_STATS_PER
+#define ARROW_STATS_PER 4
+#endif
+constexpr int kPer = ARROW_STATS_PER;   // requests per lane per chunk (one ring stage)
 constexpr int kChunk = 32 * kPer;
 constexpr int kWarps = kStatsThreads / 32;
 constexpr int kBins = ARROW_STATS_HIST_BINS;
@@ -130,13 +133,15 @@ __device__ void warp_merge(Acc& a) {
   }
 }
 
-// hist[off + v - 1] += 1 for v in 1..kBins, else the spare word after both
-// histograms: one unconditional red.shared on a shared-window address (no
-// branch, no generic-to-shared conversion per update).
-constexpr int kHistWords = 2 * kBins + 32;  // + spare (keeps the ring 128 B aligned)
-__device__ __forceinline__ void hist_inc(uint32_t hist_sa, int32_t v, int off) {
-  const uint32_t b = (uint32_t)(v - 1);
-  const uint32_t idx = b < (uint32_t)kBins ? (uint32_t)off + b : (uint32_t)(2 * kBins);
+// Each histogram is kBins + 2 words indexed by the length itself: word v for
+// v in 1..kBins, word 0 (v == 0) and word kBins + 1 (v > kBins, or v < 0 as
+// unsigned) are spares the copy-out skips.  One unsigned min, one address
+// and one unconditional red.shared per update (no branch, no generic-to-
+// shared conversion).
+constexpr int kHistSpan = kBins + 2;
+constexpr int kHistWords = (2 * kHistSpan + 31) / 32 * 32;  // keeps the ring 128 B aligned
+__device__ __forceinline__ void hist_inc(uint32_t hist_sa, int32_t v) {
+  const uint32_t idx = min((uint32_t)v, (uint32_t)(kBins + 1));
   asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hist_sa + 4u * idx) : "memory");
 }
 
@@ -214,7 +219,8 @@ __device__ __forceinline__ void fold_chunk(const arrow_stats_args_t& A, Acc& acc
                                            const Chunk& c, int64_t base, int64_t end, int lane, double lo_d,
                                            double hi_d, double inv_b) {
   const double w = A.bucket_s;
-  const uint32_t hist_sa = (uint32_t)__cvta_generic_to_shared(hist);
+  const uint32_t hist_sx = (uint32_t)__cvta_generic_to_shared(hist);
+  const uint32_t hist_sy = hist_sx + 4u * kHistSpan;
   uint64_t qxx = 0, qyy = 0, qxy = 0;
   uint32_t big = 0;
 #pragma unroll
@@ -251,13 +257,15 @@ __device__ __forceinline__ void fold_chunk(const arrow_stats_args_t& A, Acc& acc
       }
     }
     if (v) {
-      acc.tmin = t < acc.tmin ? t : acc.tmin;  // arrivals are never NaN
-      acc.tmax = t > acc.tmax ? t : acc.tmax;
+      // arrivals are never NaN; a +-0 tie may keep either zero (only the
+      // duration max - min is used)
+      acc.tmin = fmin(t, acc.tmin);
+      acc.tmax = fmax(t, acc.tmax);
       // predicated shared-memory reductions on precomputed shared-window
       // addresses (lengths outside 1..kBins are counted on the host as
       // n - sum(bins))
-      hist_inc(hist_sa, x, 0);
-      hist_inc(hist_sa, y, kBins);
+      hist_inc(hist_sx, x);
+      hist_inc(hist_sy, y);
     }
     const uint64_t ux = (uint32_t)x, uy = (uint32_t)y;
     big |= (uint32_t)x | (uint32_t)y;
@@ -343,7 +351,7 @@ __device__ __forceinline__ void issue_stage(const arrow_stats_args_t& A, Stage* 
 
 __global__ void __launch_bounds__(kStatsThreads, 1) arrow_stats_kernel(const arrow_stats_args_t A) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  uint32_t* hist = (uint32_t*)smem_raw;  // [2][kBins]
+  uint32_t* hist = (uint32_t*)smem_raw;  // [2][kHistSpan]
   __shared__ Acc red[kWarps];
   __shared__ uint64_t bars[kWarps][kStages];
   for (int i = threadIdx.x; i < kHistWords; i += blockDim.x) hist[i] = 0;
@@ -380,9 +388,9 @@ __global__ void __launch_bounds__(kStatsThreads, 1) arrow_stats_kernel(const arr
       for (int q = 0; q < kStages && q < nfull; q++) issue_stage(A, &ring[q], &bar[q], begin + (int64_t)q * kChunk);
     }
     __syncwarp();
+    int q = 0;             // stage of chunk j
+    uint32_t parity = 0;   // phase of that stage's barrier
     for (int64_t j = 0; j < nfull; j++) {
-      const int q = (int)(j % kStages);
-      const uint32_t parity = (uint32_t)((j / kStages) & 1);
       while (!mbar_try_wait(&bar[q], parity)) {
       }
       Chunk c;
@@ -398,6 +406,10 @@ __global__ void __launch_bounds__(kStatsThreads, 1) arrow_stats_kernel(const arr
         issue_stage(A, &ring[q], &bar[q], begin + (j + kStages) * kChunk);
       }
       fold_chunk<true>(A, acc, run, hist, c, begin + j * kChunk, end, lane, lo_d, hi_d, inv_b);
+      if (++q == kStages) {
+        q = 0;
+        parity ^= 1u;
+      }
     }
     const int64_t tail = begin + nfull * kChunk;
     if (tail < end) {
@@ -427,8 +439,9 @@ __global__ void __launch_bounds__(kStatsThreads, 1) arrow_stats_kernel(const arr
   if (lane == 0) red[warp] = acc;
   __syncthreads();
   for (int i = threadIdx.x; i < kBins; i += blockDim.x) {
-    if (hist[i]) atomicAdd(&A.hist_x[i], hist[i]);
-    if (hist[kBins + i]) atomicAdd(&A.hist_y[i], hist[kBins + i]);
+    const uint32_t hx = hist[1 + i], hy = hist[kHistSpan + 1 + i];
+    if (hx) atomicAdd(&A.hist_x[i], hx);
+    if (hy) atomicAdd(&A.hist_y[i], hy);
   }
   if (threadIdx.x == 0) {
     Acc a = red[0];
