@@ -223,16 +223,24 @@ __device__ __forceinline__ void fold_chunk(const arrow_stats_args_t& A, Acc& acc
   const uint32_t hist_sy = hist_sx + 4u * kHistSpan;
   uint64_t qxx = 0, qyy = 0, qxy = 0;
   uint32_t big = 0;
+  // Still in the run's bucket F?  For t >= 0 the bucket is trunc(t / w)
+  // (see floordiv_fast), so t is in F iff F*w <= t < (F+1)*w, decided
+  // exactly by the signs of two FMA residuals.  One vote for the whole
+  // chunk: the common case (the chunk stays in the run) is branch-free.
+  bool chunk_in = true;
+#pragma unroll
+  for (int k = 0; k < kPer; k++) {
+    const bool v = kFull || base + lane + 32 * k < end;
+    const double t = c.t[k];
+    chunk_in = chunk_in && (!v || (fma(-run.f, w, t) >= 0.0 && fma(-run.f1, w, t) < 0.0));
+  }
+  chunk_in = __all_sync(FULL, chunk_in);
 #pragma unroll
   for (int k = 0; k < kPer; k++) {
     const bool v = kFull || base + lane + 32 * k < end;
     const double t = c.t[k];
     const int32_t x = c.x[k], y = c.y[k];
-    // Still in the run's bucket F?  For t >= 0 the bucket is trunc(t / w)
-    // (see floordiv_fast), so t is in F iff F*w <= t < (F+1)*w, decided
-    // exactly by the signs of two FMA residuals.
-    const bool in_run = fma(-run.f, w, t) >= 0.0 && fma(-run.f1, w, t) < 0.0;
-    if (__all_sync(FULL, !v || in_run)) {
+    if (chunk_in || __all_sync(FULL, !v || (fma(-run.f, w, t) >= 0.0 && fma(-run.f1, w, t) < 0.0))) {
       run.c += v ? 1u : 0u;
       run.x += (uint32_t)x;  // 0 on padding lanes
       run.y += (uint32_t)y;
