@@ -235,6 +235,22 @@ __device__ __forceinline__ void fold_chunk(const arrow_stats_args_t& A, Acc& acc
     chunk_in = chunk_in && (!v || (fma(-run.f, w, t) >= 0.0 && fma(-run.f1, w, t) < 0.0));
   }
   chunk_in = __all_sync(FULL, chunk_in);
+  if (kFull) {
+    // arrival extremes as a tree (arrivals are never NaN; a +-0 tie may keep
+    // either zero, only the duration max - min is used)
+    double lo[kPer], hi[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; k++) lo[k] = hi[k] = c.t[k];
+#pragma unroll
+    for (int d = 1; d < kPer; d *= 2)
+#pragma unroll
+      for (int k = 0; k + d < kPer; k += 2 * d) {
+        lo[k] = fmin(lo[k], lo[k + d]);
+        hi[k] = fmax(hi[k], hi[k + d]);
+      }
+    acc.tmin = fmin(lo[0], acc.tmin);
+    acc.tmax = fmax(hi[0], acc.tmax);
+  }
 #pragma unroll
   for (int k = 0; k < kPer; k++) {
     const bool v = kFull || base + lane + 32 * k < end;
@@ -265,10 +281,10 @@ __device__ __forceinline__ void fold_chunk(const arrow_stats_args_t& A, Acc& acc
       }
     }
     if (v) {
-      // arrivals are never NaN; a +-0 tie may keep either zero (only the
-      // duration max - min is used)
-      acc.tmin = fmin(t, acc.tmin);
-      acc.tmax = fmax(t, acc.tmax);
+      if (!kFull) {
+        acc.tmin = fmin(t, acc.tmin);
+        acc.tmax = fmax(t, acc.tmax);
+      }
       // predicated shared-memory reductions on precomputed shared-window
       // addresses (lengths outside 1..kBins are counted on the host as
       // n - sum(bins))
