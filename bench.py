@@ -225,17 +225,17 @@ def run_reference(args, rank: int, world: int) -> None:
 
 def measure_components() -> dict:
     """The §8(f) kernels around the evaluator, each on its own (not part of
-    the headline step): the device workload generator (rank 3, 8 192 seeds
+    the headline step): the device workload generator (rank 3, 32 768 seeds
     of the bundled bursty workload per launch) and the trace_stats scan
-    (rank 4, a 100 M-request trace resident in HBM, L2 flushed per launch),
+    (rank 4, a 200 M-request trace resident in HBM, L2 flushed per launch),
     with their CPU-reference rates on one host core for context."""
     sys.path.insert(0, str(ROOT / "scripts"))
     import bench_stats
     import bench_traces
 
     return {
-        "gen_synthetic": bench_traces.measure(8192, steps=5, warmup=2, cpu_sample=4),
-        "trace_stats": bench_stats.measure(100_000_000, steps=10, warmup=3, cpu_sample=100_000),
+        "gen_synthetic": bench_traces.measure(32768, steps=5, warmup=2, cpu_sample=4),
+        "trace_stats": bench_stats.measure(200_000_000, steps=10, warmup=3, cpu_sample=100_000),
     }
 
 
