@@ -1650,6 +1650,7 @@ struct Sim {
     uint32_t key2[IPL];
     bool pushed[IPL];
     int completed = 0, n_part = 0;
+    PROF_CLOCK(pr0);
 #pragma unroll
     for (int k = 0; k < IPL; k++) {
       pushed[k] = false;
@@ -1662,6 +1663,11 @@ struct Sim {
       n_part++;
       iteration_complete<false>(I, I.busy_until, completed, pushed[k]);
     }
+#ifdef ARROW_PROF
+    w.sync();
+#endif
+    PROF_MARK(0, pr0);
+    PROF_CLOCK(pr1);
     // exact push sequence: the round's pushes, in (time, seq) order of the
     // events that made them, continue the global counter
     const uint32_t base = u().seq;
@@ -1682,6 +1688,7 @@ struct Sim {
           if (pushed[k] && (a < key1[k] || (a == key1[k] && b < key2[k]))) pre[k]++;
       }
     }
+    PROF_MARK(1, pr1);
     Head loud;
     loud.code = -1;
     loud.k = ~0ull;

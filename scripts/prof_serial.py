@@ -30,7 +30,7 @@ def main():
     rc = lib.arrow_sim_prof(out.ctypes.data_as(ctypes.c_void_p), len(scen))
     assert rc == 0, rc
     p = out.reshape(-1, 16)
-    names = ["-", "-", "prefill_c", "arrival", "tick", "loud_iter", "migration", "rescan", "burst_sel", "burst_run", "round_sel", "round_run", "chains", "merge", "delays", "load_low"]
+    names = ["rr_iter", "rr_rank", "prefill_c", "arrival", "tick", "loud_iter", "migration", "rescan", "burst_sel", "burst_run", "round_sel", "round_run", "chains", "merge", "delays", "load_low"]
     cyc = hb.summaries["cycles"]
     top = np.argsort(-cyc)[:6]
     for k in top:
