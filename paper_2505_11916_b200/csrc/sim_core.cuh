@@ -372,8 +372,8 @@ struct Sim {
   AS_HD int warp_argmin(uint64_t key, uint32_t tie, bool valid) {
     // each stage stops as soon as a single lane is left
     uint32_t b = w.ballot(valid);
+    const uint32_t hi = w.min_u32(valid ? (uint32_t)(key >> 32) : ~0u);  // issued with the ballot
     if ((b & (b - 1)) == 0) return b ? ffs32(b) : -1;
-    const uint32_t hi = w.min_u32(valid ? (uint32_t)(key >> 32) : ~0u);
     bool m = valid && (uint32_t)(key >> 32) == hi;
     b = w.ballot(m);
     if ((b & (b - 1)) == 0) return ffs32(b);
@@ -1784,8 +1784,9 @@ struct Sim {
       any_safe = any_safe || safe[k];
       if (I.id >= 0 && I.busy && !safe[k] && (uint32_t)(I.ck >> 32) < ns_hi) ns_hi = (uint32_t)(I.ck >> 32);
     }
-    if (!w.any(any_safe)) return false;
+    const bool some_safe = w.any(any_safe);
     ns_hi = w.min_u32(ns_hi);
+    if (!some_safe) return false;
     // limit = min(serial head, non-safe events rounded down to their high word)
     uint64_t lim_k = ~0ull;
     uint32_t lim_s = ~0u;
@@ -1812,9 +1813,10 @@ struct Sim {
         if ((uint32_t)(I.ck >> 32) < t_hi) t_hi = (uint32_t)(I.ck >> 32);
       }
     }
+    // both reductions issued back to back (independent), then the test
     const uint32_t n_part = w.add_u32((uint32_t)n_mine);
-    if (n_part == 0) return false;
     t_hi = w.min_u32(t_hi);
+    if (n_part == 0) return false;
     per = (int)(BURST_POOL / n_part);
     if (per > BURST_MAX) per = BURST_MAX;
     // at most `per` events per instance: decode-only iterations last >= b1 + b0
