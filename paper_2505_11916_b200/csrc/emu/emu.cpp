@@ -91,6 +91,15 @@ struct EmuWarp {
   uint32_t add_u32(uint32_t v) const {
     return (uint32_t)fold(v, [](uint64_t a, uint64_t b) { return (uint64_t)(uint32_t)(a + b); });
   }
+  uint32_t match_any(uint64_t v) const {
+    sh->slot[ln] = v;
+    sync();
+    uint32_t m = 0;
+    for (int i = 0; i < WIDTH; i++)
+      if (sh->slot[i] == v) m |= 1u << i;
+    sync();
+    return m;
+  }
   int atomic_add_shared(int* p, int v) const { return __atomic_fetch_add(p, v, __ATOMIC_RELAXED); }
 };
 

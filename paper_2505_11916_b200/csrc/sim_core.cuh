@@ -2114,6 +2114,25 @@ struct Sim {
     // equal final times fall back to the sequential merge below, which
     // reproduces the full (time, seq) order.
     int before[IPL];
+    if (IPL == 1) {
+      // Sharper still: the finals' relative order only matters among
+      // finals whose pushed events have equal times.  When every pushed
+      // event time is distinct (one match), lane order is as good as rank
+      // order and the merge is two votes.
+      const bool fin = safe[0] && lastp[0];
+      const uint64_t nk = fin ? tkey(st[0].busy_until) : (uint64_t)lane;  // dummies: sign bit clear
+      const uint32_t peers = w.match_any(nk);
+      const uint32_t fm = w.ballot(fin);
+      const bool dup = w.any(fin && (peers & (peers - 1u)) != 0);
+      if (!dup) {
+        const uint32_t packed = w.add_u32((uint32_t)events | ((uint32_t)completed << 16));
+        const uint32_t total_push = w.add_u32((uint32_t)pushes);
+        if (fin) st[0].iter_seq = base + total_push - (uint32_t)popc32(fm) + (uint32_t)popc32(fm & ((1u << lane) - 1u));
+        PROF_MARK(13, pb1);
+        burst_finish(safe, base, packed, total_push, h);
+        return;
+      }
+    }
     uint64_t xlast[IPL];  // key of each chain's final (pending-push) event
 #pragma unroll
     for (int k = 0; k < IPL; k++) {
@@ -2192,7 +2211,12 @@ struct Sim {
         if (safe[k] && lastp[k]) st[k].iter_seq = sm->bseq[st[k].id];
     }
     PROF_MARK(13, pb1);
-    // a chain stopped at its migration bound leaves a loud pending event
+    burst_finish(safe, base, packed, total_push, h);
+  }
+
+  // a chain stopped at its migration bound leaves a loud pending event;
+  // counters
+  AS_HD void burst_finish(const bool safe[IPL], uint32_t base, uint32_t packed, uint32_t total_push, Head& h) {
     Head loud;
     loud.code = -1;
     loud.k = ~0ull;
