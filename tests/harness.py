@@ -185,3 +185,40 @@ def golden_free_decisions(hb: HostBuffers, s: int, cb) -> list[dict]:
     from paper_2505_11916_b200 import _results
 
     return _results.decision_dicts(hb, s, cb.table.entries[cb.trace_index[s]].ids)
+
+
+def lockstep_scenarios():
+    """Groups of identical requests arriving at the same instant on eight
+    identical instances: dispatch, batches and iteration times coincide
+    across instances, so many events share exact times and the (time, kind,
+    seq) tie-breaks decide the order.  One scenario per policy."""
+    from paper_2505_11916_b200 import workloads as W
+    from paper_2505_11916_b200._compile import Scenario
+    from paper_2505_11916_b200.core import TraceRequest
+
+    trace = []
+    for g in range(12):
+        for j in range(8):
+            trace.append(TraceRequest(len(trace), 0.25 * g, 64 + 32 * (g % 3), 24 + 8 * (g % 2)))
+    base = W.sweep_base(8)
+    return [Scenario(trace, W.policy_config(base, p, 8), 1.0, p) for p in W.POLICIES]
+
+
+def assert_same_run(got, exp, n: int) -> None:
+    """Every summary field, per-request time and dispatch target equal."""
+    from paper_2505_11916_b200 import _abi
+
+    for s in range(n):
+        g, e = got.summaries[s], exp.summaries[s]
+        for f in ("status", "n_completed", "n_ok", "n_flips", "n_events", "n_iterations", "n_decisions",
+                  "n_ticks", "decision_hash"):
+            assert int(g[f]) == int(e[f]), (s, f, g[f], e[f])
+        for f in ("stall_time", "attainment", "p90_ttft", "p90_tpot", "mean_ttft", "mean_tpot", "goodput", "span"):
+            assert_same_f64([g[f]], [e[f]], f"scenario {s} {f}")
+    assert_same_f64(got.req_first, exp.req_first, "first")
+    for s in range(n):
+        if int(exp.summaries[s]["status"]) == _abi.OK:
+            sl = got.req_slice(s)
+            assert_same_f64(got.req_last[sl], exp.req_last[sl], f"scenario {s} last")
+    np.testing.assert_array_equal(got.req_prefill, exp.req_prefill)
+    np.testing.assert_array_equal(got.req_decode, exp.req_decode)

@@ -100,3 +100,17 @@ def test_emulated_kernel_without_iteration_log(meta):
     cb = H.compile_golden([(meta, arrays)])
     hb = H.run_emu(cb, NO_ITERLOG, width=8)
     H.check_vs_golden(meta, arrays, hb)
+
+
+def test_emulated_kernel_lockstep_instances_match_oracle():
+    """Simultaneous identical requests on identical instances: exact ties
+    between event times (tests/harness.py: lockstep_scenarios)."""
+    from paper_2505_11916_b200._buffers import OutputSpec
+    from paper_2505_11916_b200._compile import compile_batch
+
+    cb = compile_batch(H.lockstep_scenarios(), 500_000)
+    spec = OutputSpec(requests=True)
+    got = H.run_emu(cb, spec, width=8)
+    exp = H.run_oracle(cb, spec)
+    H.assert_same_run(got, exp, cb.n)
+    assert (exp.summaries["status"] == 0).all()

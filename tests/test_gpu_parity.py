@@ -162,3 +162,15 @@ def test_both_kernel_builds_bit_exact(build):
         for f in ("status", "n_completed", "n_ok", "n_flips", "n_events", "n_decisions", "decision_hash"):
             assert int(got.summaries[s][f]) == int(exp.summaries[s][f]), (build, s, f)
     np.testing.assert_array_equal(got.req_prefill, exp.req_prefill)
+
+
+def test_lockstep_instances_match_oracle(evaluator):
+    """Simultaneous identical requests on identical instances (exact event
+    time ties), both kernel builds, against the CPU oracle."""
+    from paper_2505_11916_b200._backend import CudaEvaluator
+
+    cb = compile_batch(H.lockstep_scenarios(), 500_000)
+    spec = OutputSpec(requests=True)
+    exp = H.run_oracle(cb, spec)
+    for ev in (evaluator, CudaEvaluator(build="throughput")):
+        H.assert_same_run(ev.execute(cb, spec), exp, cb.n)
