@@ -24,7 +24,10 @@ constexpr int kThreads = kWarpsPerBlock * 32;
 // resident warps finishes when its longest scenario does); MINB = 3 caps
 // registers at 168 so three blocks (12 warps) share an SM (throughput for
 // sweeps of many waves, where issue slots, not chain latency, are the bound).
-constexpr int kMinBlocksThroughput = 3;
+#ifndef ARROW_TP_BLOCKS
+#define ARROW_TP_BLOCKS 3
+#endif
+constexpr int kMinBlocksThroughput = ARROW_TP_BLOCKS;
 constexpr int kLatWarps = ARROW_LAT_WARPS;  // warps per block of the latency build
 
 template <int IPL, int MINB, int WPB>
