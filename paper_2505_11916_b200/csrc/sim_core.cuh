@@ -213,6 +213,7 @@ struct Inst {
   double dly;                   // predicted_prefill_delay at the current event (exact iff dexact)
   double dlo, dhi;              // interval certainly holding the exact predicted_prefill_delay
   int dexact;                   // dly is the exact left fold
+  int pool;                     // register copy of sm->pool_of[id] (owner lane)
   double ws_hi, ws_lo;          // waiting-prefill terms: double-double running sum ...
   double ws_max;                // ... and the largest |term| since the queue was last empty
 };
@@ -839,7 +840,7 @@ struct Sim {
     if (nd + npf > 0) emit(I, now);
     // _check_drained (engine.py:183-192): decided here, applied by the warp
     int dst = -1;
-    int pk = pool_of(I.id);
+    int pk = I.pool;
     if (pk == P_P2D && !has_prefill_work(I))
       dst = P_DECODE;
     else if (pk == P_D2P && !has_decode_work(I))
@@ -908,6 +909,9 @@ struct Sim {
       U.n_flips++;
       log_decision(now, ARROW_DEC_FLIP, -1, id, trigger | (src << 3) | (dst << 5));
     });
+#pragma unroll
+    for (int k = 0; k < IPL; k++)
+      if (st[k].id == id) st[k].pool = dst;
   }
 
   // ---------------------------------------------------- scheduler ------
@@ -926,7 +930,7 @@ struct Sim {
 
   // _argmin over one pool (insertion order), key = delay
   AS_HD int argmin_delay_pool(int pool) {
-    return argmin_delay([&](const Inst& I) { return pool_of(I.id) == pool; },
+    return argmin_delay([&](const Inst& I) { return I.pool == pool; },
                         [&](const Inst& I) { return (uint32_t)pos_of(I.id); });
   }
 
@@ -1000,7 +1004,7 @@ struct Sim {
 
   AS_HD int argmin_tokens_pool(int pool) {
     return argmin_inst([&](Inst& I, uint64_t& key, uint32_t& tie) {
-      if (pool_of(I.id) != pool) return false;
+      if (I.pool != pool) return false;
       key = (uint64_t)(uint32_t)I.rtok;
       tie = (uint32_t)pos_of(I.id);
       return true;
@@ -1479,6 +1483,7 @@ struct Sim {
       I.rp_rid = -1;
       I.min_f = 0x7fffffff;
       I.mig_rid = -1;
+      I.pool = I.id >= 0 ? pool_of(I.id) : -1;
     }
     int32_t* rpf = (have_om && om.req_offset >= 0) ? B->req_prefill : 0;
     int32_t* rdc = (have_om && om.req_offset >= 0) ? B->req_decode : 0;
@@ -1529,7 +1534,7 @@ struct Sim {
       const int freed = (fin > 0 ? I.held_min : 0) + I.pb_rel;
       if (x + freed >= I.mq_need) return false;
     }
-    const int pk = pool_of(I.id);
+    const int pk = I.pool;
     if (pk == P_P2D)
       return I.wp_c > I.pb_k || I.pb_rp_left || (I.pb_k > 0 && !I.pb_last_comp);
     if (pk == P_D2P) return I.mig_active || I.mq_c > 0 || I.wd_c > 0 || I.R - fin > 0;
@@ -1744,7 +1749,7 @@ struct Sim {
   // after the last kick, which would change R and min_f: such chains only
   // run when no migration can be pending.)
   AS_HD bool chain_safe(const Inst& I) const {
-    const int pk = pool_of(I.id);
+    const int pk = I.pool;
     return I.busy && I.cq && I.rp_rid < 0 && I.wp_c == 0 && (pk == P_PREFILL || pk == P_DECODE) &&
            !(I.mq_c > 0 && !I.mig_active && I.wd_c > 0);
   }
