@@ -238,6 +238,14 @@ AS_HD uint64_t okey(double x) {
 // of okey's sign select and canonicalising add.
 AS_HD uint64_t tkey(double t) { return dbits(t) | 0x8000000000000000ull; }
 
+// Inverse of tkey (keys of event times, sign bit always set).
+AS_HD double tkey_inv(uint64_t k) {
+  const uint64_t u = k & 0x7fffffffffffffffull;
+  double x;
+  memcpy(&x, &u, 8);
+  return x;
+}
+
 AS_HD double okey_inv(uint64_t k) {
   uint64_t u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
   double x;
@@ -1826,7 +1834,7 @@ struct Sim {
     if (per > BURST_MAX) per = BURST_MAX;
     // at most `per` events per instance: decode-only iterations last >= b1 + b0
     // (t0 <= the earliest participant's time)
-    const double t0 = okey_inv((uint64_t)t_hi << 32);
+    const double t0 = tkey_inv((uint64_t)t_hi << 32);
     uint64_t cap = tkey(t0 + (double)(per - 4) * (sc().b1 + sc().b0));
     {
       uint32_t l_hi = ~0u;
@@ -2296,7 +2304,7 @@ struct Sim {
       PROF_MARK(8, c0);
       if (h.code < 0) break;
       const int ev = h.code;
-      double now = okey_inv(h.k);
+      double now = tkey_inv(h.k);
       lane0([&] {
         u().now = now;
         u().esp++;
