@@ -92,12 +92,23 @@ struct Acc {
   double tmin, tmax;
   int64_t count, sx, sy, oow;
   U128 sxx, syy, sxy;
+  uint64_t pxx, pyy, pxy;  // pending 64-bit moments of up to 32/kPer chunks
+  int pn;
 
   __device__ void init() {
     tmin = INFINITY;
     tmax = -INFINITY;
     count = sx = sy = oow = 0;
     sxx = syy = sxy = U128{0, 0};
+    pxx = pyy = pxy = 0;
+    pn = 0;
+  }
+  __device__ void flush_pending() {
+    sxx.add(pxx);
+    syy.add(pyy);
+    sxy.add(pxy);
+    pxx = pyy = pxy = 0;
+    pn = 0;
   }
   __device__ void merge(const Acc& o) {
     tmin = fmin(tmin, o.tmin);
@@ -298,9 +309,10 @@ __device__ __forceinline__ void fold_chunk(const arrow_stats_args_t& A, Acc& acc
     qxy += ux * uy;
   }
   if (big < (1u << 29)) {
-    acc.sxx.add(qxx);
-    acc.syy.add(qyy);
-    acc.sxy.add(qxy);
+    acc.pxx += qxx;
+    acc.pyy += qyy;
+    acc.pxy += qxy;
+    if (++acc.pn == 32 / kPer) acc.flush_pending();  // 32/kPer chunks of < kPer * 2^58 stay below 2^63
   } else {  // huge lengths: redo this chunk's moments with a carry per term
 #pragma unroll
     for (int k = 0; k < kPer; k++) {
@@ -459,6 +471,7 @@ __global__ void __launch_bounds__(kStatsThreads, 1) arrow_stats_kernel(const arr
     }
   }
   run.flush(A, acc, lo_d, lane);
+  acc.flush_pending();
   warp_merge(acc);
   if (lane == 0) red[warp] = acc;
   __syncthreads();
