@@ -26,7 +26,7 @@ $(LIB): $(SRCS) $(HDRS)
 oracle:
 	$(MAKE) -s -C oracle
 
-emu: build/libarrow_emu.so build/libarrow_emu_wide.so build/libnpgen_host.so
+emu: build/libarrow_emu.so build/libarrow_emu_wide.so build/libarrow_emu_mut.so build/libnpgen_host.so
 
 build/libarrow_emu.so: $(CSRC)/emu/emu.cpp $(HDRS)
 	@mkdir -p build
@@ -39,6 +39,13 @@ build/libarrow_emu_wide.so: $(CSRC)/emu/emu.cpp $(HDRS)
 	@mkdir -p build
 	$(CXX_HOST) -std=c++20 -O2 -g -fPIC -shared -ffp-contract=off -fno-fast-math -pthread \
 		-Wall -Wno-unknown-pragmas -DARROW_DELAY_SLACK=0x1p-12 -Iinclude -o $@ $(CSRC)/emu/emu.cpp
+
+# test-only mutant: the burst merge's equal-time fallback in reversed order
+# (tests prove the tie fixture can tell it from the shipped source)
+build/libarrow_emu_mut.so: $(CSRC)/emu/emu.cpp $(HDRS)
+	@mkdir -p build
+	$(CXX_HOST) -std=c++20 -O2 -g -fPIC -shared -ffp-contract=off -fno-fast-math -pthread \
+		-Wall -Wno-unknown-pragmas -DARROW_MUTATE_TIE_REVERSE -Iinclude -o $@ $(CSRC)/emu/emu.cpp
 
 build/libnpgen_host.so: $(CSRC)/emu/npgen_host.cpp $(HDRS)
 	@mkdir -p build

@@ -30,7 +30,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent))
 
 import pdsim  # noqa: E402
 import pdsim.engine as engine_module  # noqa: E402
-from scenarios import catalogue  # noqa: E402
+from scenarios import catalogue, catalogue_r2  # noqa: E402
 
 OUT = Path(__file__).resolve().parents[1] / "tests" / "golden"
 
@@ -99,10 +99,11 @@ def run_one(sc):
         recs = result.records
         arrays["first"] = np.array([r.token_times[0] for r in recs])
         arrays["last"] = np.array([r.token_times[-1] for r in recs])
-        arrays["ntok"] = np.array([len(r.token_times) for r in recs], dtype=np.int64)
         arrays["flags"] = np.array([r.ttft_ok | (r.tpot_ok << 1) | (r.slo_ok << 2) for r in recs], dtype=np.uint8)
-        arrays["ttft"] = np.array([r.ttft for r in recs])
-        arrays["tpot"] = np.array([r.tpot for r in recs])
+        if not sc.get("compact"):
+            arrays["ntok"] = np.array([len(r.token_times) for r in recs], dtype=np.int64)
+            arrays["ttft"] = np.array([r.ttft for r in recs])
+            arrays["tpot"] = np.array([r.tpot for r in recs])
         arrays["transitions"] = np.array([(i, POOL[a.value], POOL[b.value]) for i, a, b in result.transitions],
                                          dtype=np.int32).reshape(-1, 3)
         if sc["full"]:
@@ -174,18 +175,35 @@ def known_answers():
 
 
 def main():
+    """GOLDEN_SET=r1 (default): the round-1 catalogue, rewriting index.json.
+    GOLDEN_SET=r2[:c3,c4,c5,tie]: the BASELINE C3/C4/C5 scenarios and the
+    burst-merge tie case (scenarios.catalogue_r2), merged into index.json by
+    name; their fixtures are compact (no ttft/tpot/ntok arrays: those follow
+    from first/last token times and output_len)."""
     OUT.mkdir(parents=True, exist_ok=True)
     include_slow = os.environ.get("GOLDEN_FAST") != "1"
+    which = os.environ.get("GOLDEN_SET", "r1")
     index = []
     t_all = time.perf_counter()
-    for sc in catalogue(make, include_slow=include_slow):
+    if which.startswith("r2"):
+        parts = tuple(which.split(":", 1)[1].split(",")) if ":" in which else ("c3", "c4", "c5", "tie")
+        scs = catalogue_r2(make, which=parts)
+        for sc in scs:
+            sc["compact"] = not sc["full"]
+        old = json.loads((OUT / "index.json").read_text())
+        names = {sc["name"] for sc in scs}
+        index = [m for m in old["scenarios"] if m["name"] not in names]
+    else:
+        scs = catalogue(make, include_slow=include_slow)
+    for sc in scs:
         meta, arrays = run_one(sc)
         fname = f"{sc['name']}.npz"
         np.savez_compressed(OUT / fname, **arrays)
         meta["file"] = fname
         index.append(meta)
         print(f"{sc['name']:28s} n={len(sc['trace']):5d} {meta['wall_s']:7.2f}s err={meta['error']}", flush=True)
-    np.savez_compressed(OUT / "known_answers.npz", **known_answers())
+    if not which.startswith("r2"):
+        np.savez_compressed(OUT / "known_answers.npz", **known_answers())
     (OUT / "index.json").write_text(json.dumps(dict(
         generator="oracle/gen_golden.py",
         reference="/root/reference/pkg/src (pdsim)",

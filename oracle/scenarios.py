@@ -234,3 +234,148 @@ def catalogue(make, include_slow=True):
         rate = float(rng.choice([1.0, 3.0, 6.0, 12.0])) * max(N, 1) / 4
         add(f"fuzz_{k:02d}", tr, v, scale=rate_scale(tr, rate), stall_limit=20000, full=k % 3 == 0)
     return S
+
+
+# ---------------------------------------------------------------------------
+# BASELINE configs C3, C4, C5 and the burst-merge tie case.
+# Generated into tests/golden/ with GOLDEN_SET=r2 (oracle/gen_golden.py).
+
+def code_like(make):
+    """C3 code-like trace: 3 955 requests."""
+    return synthetic(make, 600.0, 4.0, math.log(1500.0), 0.9, math.log(40.0), 0.8,
+                     ((60.0, 30.0, 5.0), (240.0, 45.0, 4.0), (450.0, 30.0, 6.0)), 8000, 1000, 101)
+
+
+def conversation_like(make):
+    """C3 conversation-like trace: 3 133 requests."""
+    return synthetic(make, 600.0, 4.0, math.log(800.0), 0.8, math.log(250.0), 0.6,
+                     ((120.0, 120.0, 1.5), (360.0, 120.0, 2.0)), 8000, 2000, 202)
+
+
+def c4_trace(make):
+    """C4 trace: 10 000 requests."""
+    return synthetic(make, 3600.0, 4.0, math.log(420.0), 0.55, math.log(130.0), 0.5,
+                     ((600.0, 120.0, 5.0), (1800.0, 180.0, 4.0)), 3500, 900, 3)[:10000]
+
+
+def policy_values(policy, n, **kw):
+    """Arrow / static PD / PD-colocated as flat config values
+    (paper_2505_11916_b200/workloads.py:policy_config, restated)."""
+    if policy == "arrow":
+        v = cfg(instances=n, strategy="slo-aware", init_prefill=n // 2, init_decode=n - n // 2)
+    elif policy == "static-pd":
+        v = cfg(instances=n, strategy="minimal-load", init_prefill=n // 2, init_decode=n - n // 2)
+    elif policy == "colocated":
+        v = cfg(instances=n, strategy="slo-aware", enable_flips=False, init_prefill=n, init_decode=0)
+    else:
+        raise ValueError(policy)
+    v.update(kw)
+    return v
+
+
+C3_POINTS = (  # (ttft_slo, tpot_slo, rate): six points of the 8 x 5 SLO grid, rates 2..16
+    (0.25, 0.025, 4.0), (0.5, 0.05, 8.0), (1.0, 0.075, 12.0), (2.0, 0.1, 16.0), (5.0, 0.15, 6.0), (30.0, 0.025, 10.0),
+)
+
+C4_POINTS = (  # (N, theta_d, theta_busy, breach, ttft_threshold factor, rate factor)
+    (16, 0.25, 0.5, 1.0, 0.5, 1.25), (16, 1.0, 0.9, 4.0, 1.0, 2.5), (24, 0.5, 0.75, 2.0, 0.75, 2.5),
+    (32, 0.25, 0.9, 4.0, 1.0, 1.25), (32, 1.0, 0.5, 1.0, 0.5, 2.5), (48, 0.75, 0.75, 2.0, 0.75, 1.25),
+    (48, 0.25, 0.5, 4.0, 0.5, 2.5), (64, 1.0, 0.9, 1.0, 1.0, 2.5), (64, 0.5, 0.5, 2.0, 0.75, 1.25),
+)
+
+C5_RADIX = (4, 32, 3, 4, 4, 4, 4)  # trace, rate k, policy, N, theta_d, theta_busy, breach
+C5_POLICIES = ("arrow", "static-pd", "colocated")
+C5_N = (4, 8, 16, 32)
+C5_THETA_D = (0.25, 0.5, 0.75, 1.0)
+C5_THETA_BUSY = (0.5, 0.75, 0.9, 1.0)
+C5_BREACH = (1.0, 2.0, 4.0, 8.0)
+
+
+def c5_digits(sid):
+    out = []
+    for r in C5_RADIX:
+        out.append(sid % r)
+        sid //= r
+    return out
+
+
+def c5_id(tr, k, pol, ni, td, tb, br):
+    sid = 0
+    for d, r in zip(reversed((tr, k, pol, ni, td, tb, br)), reversed(C5_RADIX)):
+        sid = sid * r + d
+    return sid
+
+
+def c5_stratified_ids(count=32, seed=55):
+    """Every trace, policy and N appear; rate and threshold digits seeded."""
+    rng = np.random.default_rng(seed)
+    ids = []
+    for j in range(count):
+        tr, pol, ni = j % 4, j % 3, (j // 4) % 4
+        k = int(rng.integers(0, 32))
+        td, tb, br = (int(x) for x in rng.integers(0, 4, size=3))
+        ids.append(c5_id(tr, k, pol, ni, td, tb, br))
+    return ids
+
+
+def c5_scenario(make, sid, traces=None):
+    """Scenario id -> (trace, config values, scale), SURVEY.md §8(d) C5."""
+    tr, k, pol, ni, td, tb, br = c5_digits(sid)
+    if traces is None:
+        traces = [bursty(make), code_like(make), conversation_like(make), ramp(make)]
+    trace = traces[tr]
+    n = C5_N[ni]
+    v = policy_values(C5_POLICIES[pol], n, theta_d=C5_THETA_D[td], theta_busy=C5_THETA_BUSY[tb],
+                      tpot_breach_duration_s=C5_BREACH[br])
+    rate = n * 0.25 * 16.0 ** (k / 31.0)
+    return trace, v, rate_scale(trace, rate)
+
+
+def tie_flip_trace(make):
+    """Burst-merge tie case.  Two decode instances (2 and 3) receive identical
+    decode work at the same instant, so their decode-only iteration chains run
+    in lockstep and end a burst with pending completions at exactly the same
+    time (the burst merge's equal-time fallback assigns their sequence
+    numbers).  Two long prompts then arrive while both prefill instances are
+    busy: Alg. 1 flips decode instances 2 and 3 into D_TO_P, and when their
+    tied completions drain them the two `drained` flips are logged in (time,
+    kind, seq) order -- so the order of the tied sequence numbers is visible in
+    the decision stream and in the PREFILL pool's insertion order."""
+    reqs = []
+    for j in range(4):                      # identical short requests -> identical decode work on 2 and 3
+        reqs.append((0.0, 40, 60))
+    for j in range(6):                      # long prompts: prefill instances saturate, Alg. 1 flips decodes
+        reqs.append((0.5 + 0.01 * j, 3000, 2))
+    for j in range(6):                      # later arrivals dispatched over the re-grown PREFILL pool
+        reqs.append((3.0 + 0.05 * j, 200, 3))
+    reqs.sort(key=lambda r: r[0])
+    return [make(i, a, il, ol) for i, (a, il, ol) in enumerate(reqs)]
+
+
+def catalogue_r2(make, c5_count=32, which=("c3", "c4", "c5", "tie")):
+    S = []
+
+    def add(name, trace, values, scale=1.0, stall_limit=500_000, full=False):
+        S.append(dict(name=name, trace=trace, values=values, scale=scale, stall_limit=stall_limit, full=full))
+
+    if "c3" in which:
+        for tname, tr in (("code", code_like(make)), ("chat", conversation_like(make))):
+            for pol in C5_POLICIES:
+                for p, (ttft, tpot, rate) in enumerate(C3_POINTS):
+                    add(f"c3_{tname}_{pol}_{p}", tr, policy_values(pol, 8, ttft_slo=ttft, tpot_slo=tpot),
+                        scale=rate_scale(tr, rate))
+    if "c4" in which:
+        tr = c4_trace(make)
+        for p, (n, td, tb, br, tf, rf) in enumerate(C4_POINTS):
+            v = policy_values("arrow", n, theta_d=td, theta_busy=tb, tpot_breach_duration_s=br,
+                              ttft_threshold=tf * DEFAULTS["ttft_slo"])
+            add(f"c4_{p}_n{n}", tr, v, scale=rate_scale(tr, rf * n))
+    if "c5" in which:
+        traces = [bursty(make), code_like(make), conversation_like(make), ramp(make)]
+        for sid in c5_stratified_ids(c5_count):
+            tr, v, sc = c5_scenario(make, sid, traces)
+            add(f"c5_{sid:05d}", tr, v, scale=sc)
+    if "tie" in which:
+        v = cfg(instances=4, init_prefill=2, init_decode=2, **ENGINE_TEST)
+        add("tie_drained_flips", tie_flip_trace(make), v, full=True)
+    return S

@@ -2190,6 +2190,7 @@ struct Sim {
       // sequential merge of all chains in (time, seq) order; bseq[i] holds
       // the sequence of chain i's current head event
       lane0([&] {
+        ATRACE("burst tie fallback base=%u\n", base);
         const int N = sc().n_instances;
         int* act = sm->list;
         int na = 0;
@@ -2206,7 +2207,11 @@ struct Sim {
           for (int a2 = 1; a2 < na; a2++) {
             const int i = act[a2];
             const uint64_t kk = sm->blist[sm->boff[i] + sm->bhead[i]];
+#ifdef ARROW_MUTATE_TIE_REVERSE  // test-only mutant: equal keys merged in reversed order
+            if (kk < bk0 || (kk == bk0 && sm->bseq[i] > sm->bseq[act[best]])) {
+#else
             if (kk < bk0 || (kk == bk0 && sm->bseq[i] < sm->bseq[act[best]])) {
+#endif
               best = a2;
               bk0 = kk;
             }

@@ -52,10 +52,13 @@ def oracle_lib() -> ctypes.CDLL:
 
 def emu_lib(variant: str = "") -> ctypes.CDLL:
     """variant "" is the kernel source as shipped; "wide" widens the delay
-    intervals so that most dispatch decisions take the exact-fold fallback."""
+    intervals so that most dispatch decisions take the exact-fold fallback;
+    "mut" merges equal-time burst finals in reversed order (a mutant the tie
+    fixture must catch)."""
     key = "emu" + variant
     if key not in _libs:
-        path = ROOT / "build" / ("libarrow_emu_wide.so" if variant == "wide" else "libarrow_emu.so")
+        path = ROOT / "build" / {"": "libarrow_emu.so", "wide": "libarrow_emu_wide.so",
+                                 "mut": "libarrow_emu_mut.so"}[variant]
         _build("emu")
         lib = ctypes.CDLL(str(path))
         lib.arrow_emu_run.argtypes = [ctypes.c_void_p, ctypes.c_int]
@@ -89,6 +92,17 @@ def compile_golden(metas_arrays, validate=True):
 
 
 FULL = OutputSpec(requests=True, decisions=True, snapshots=True, iterlog=True, diag=True)
+
+
+def spec_for(metas_arrays, base: OutputSpec = FULL) -> OutputSpec:
+    """``base`` with a decision-log capacity large enough for every fixture in
+    the group (Arrow on the C3 code-like trace logs ~2 500 flips, beyond the
+    default 2n + 64 entries)."""
+    factor = 1.0
+    for m, a in metas_arrays:
+        if "decisions" in a:
+            factor = max(factor, (len(a["decisions"]) + 64) / (2 * len(a["arrival"]) + 64))
+    return OutputSpec(**{**base.__dict__, "decision_factor": math.ceil(factor * 8) / 8})
 
 
 def run_oracle(cb, spec=FULL, threads=1, tokens=False) -> HostBuffers:

@@ -13,8 +13,14 @@ INDEX = H.golden_index()
 SMALL = [
     m
     for m in INDEX
-    if not (m["error"] and m["error"][0] == "ValueError") and not m["name"].startswith("c2_")
+    if not (m["error"] and m["error"][0] == "ValueError") and not m["name"].startswith(("c2_", "c3_", "c4_", "c5_"))
 ]
+# BASELINE C3 / C5 fixtures through the emulator: one per (trace, policy) of
+# C3 and the C5 ids with N <= 8 (the thread-per-lane emulator is slow for
+# wide clusters; every C3/C4/C5 fixture runs on the B200 in test_gpu_parity).
+R2 = [m for m in INDEX if m["name"] in (
+    "c3_code_arrow_0", "c3_code_static-pd_1", "c3_code_colocated_2", "c3_chat_arrow_3", "c3_chat_static-pd_4",
+    "c3_chat_colocated_5")] + [m for m in INDEX if m["name"].startswith("c5_") and m["values"]["instances"] <= 8]
 
 
 @pytest.mark.parametrize("meta", SMALL, ids=[m["name"] for m in SMALL])
@@ -22,6 +28,14 @@ def test_emulated_kernel_matches_reference(meta):
     arrays = H.golden_arrays(meta)
     cb = H.compile_golden([(meta, arrays)])
     hb = H.run_emu(cb, width=8)
+    H.check_vs_golden(meta, arrays, hb)
+
+
+@pytest.mark.parametrize("meta", R2, ids=[m["name"] for m in R2])
+def test_emulated_kernel_matches_reference_baseline_configs(meta):
+    arrays = H.golden_arrays(meta)
+    cb = H.compile_golden([(meta, arrays)])
+    hb = H.run_emu(cb, H.spec_for([(meta, arrays)]), width=8)
     H.check_vs_golden(meta, arrays, hb)
 
 

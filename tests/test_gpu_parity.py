@@ -39,7 +39,7 @@ def test_golden_scenarios_bit_exact(evaluator):
     checked = 0
     for group in by_limit.values():
         cb = H.compile_golden(group)
-        hb = evaluator.execute(cb, H.FULL)
+        hb = evaluator.execute(cb, H.spec_for(group))
         for s, (m, a) in enumerate(group):
             H.check_vs_golden(m, a, hb, s)
             checked += 1
@@ -151,7 +151,7 @@ def test_both_kernel_builds_bit_exact(build):
         by_limit.setdefault(m["stall_limit"], []).append((m, a))
     for group in by_limit.values():
         cb = H.compile_golden(group)
-        hb = ev.execute(cb, H.FULL)
+        hb = ev.execute(cb, H.spec_for(group))
         for s, (m, a) in enumerate(group):
             H.check_vs_golden(m, a, hb, s)
     scs = _random_scenarios(7, 48)

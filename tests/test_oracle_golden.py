@@ -23,7 +23,7 @@ INVALID = [m for m in INDEX if m["error"] and m["error"][0] == "ValueError"]
 def test_oracle_matches_reference(meta):
     arrays = H.golden_arrays(meta)
     cb = H.compile_golden([(meta, arrays)])
-    hb = H.run_oracle(cb, tokens=bool(meta["full"]))
+    hb = H.run_oracle(cb, H.spec_for([(meta, arrays)]), tokens=bool(meta["full"]))
     H.check_vs_golden(meta, arrays, hb)
     if meta["full"] and meta["error"] is None:
         got = np.concatenate([hb.tokens_of(0, r) for r in range(len(arrays["arrival"]))])
