@@ -21,6 +21,7 @@
 #include <string.h>
 
 #include <pthread.h>
+#include <time.h>
 #include <stdatomic.h>
 #include <unistd.h>
 
@@ -1215,7 +1216,14 @@ int pdsim_oracle_run_one(const arrow_batch_t* B, int s) {
 typedef struct {
   const arrow_batch_t* B;
   atomic_int next;
+  double* seconds;  /* optional: per-scenario wall seconds (bench.py's CPU baseline) */
 } pool_job_t;
+
+static double mono_now(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
 
 static void* pool_worker(void* arg) {
   pool_job_t* job = (pool_job_t*)arg;
@@ -1223,7 +1231,9 @@ static void* pool_worker(void* arg) {
     int k = atomic_fetch_add(&job->next, 1);
     if (k >= job->B->n_scenarios) break;
     int s = job->B->order ? job->B->order[k] : k;
+    const double t0 = job->seconds ? mono_now() : 0.0;
     pdsim_oracle_run_one(job->B, s);
+    if (job->seconds) job->seconds[s] = mono_now() - t0;
   }
   return NULL;
 }
@@ -1231,11 +1241,16 @@ static void* pool_worker(void* arg) {
 /* Scenarios are independent: a dynamic work queue over
  * n_threads POSIX threads, longest-first when the caller passes an order. */
 int pdsim_oracle_run_batch(const arrow_batch_t* B, int n_threads) {
+  return pdsim_oracle_run_batch_timed(B, n_threads, NULL);
+}
+
+int pdsim_oracle_run_batch_timed(const arrow_batch_t* B, int n_threads, double* seconds) {
   if (n_threads <= 0) n_threads = (int)sysconf(_SC_NPROCESSORS_ONLN);
   if (n_threads < 1) n_threads = 1;
   if (n_threads > B->n_scenarios) n_threads = B->n_scenarios > 0 ? B->n_scenarios : 1;
   pool_job_t job;
   job.B = B;
+  job.seconds = seconds;
   atomic_init(&job.next, 0);
   if (n_threads == 1) {
     pool_worker(&job);

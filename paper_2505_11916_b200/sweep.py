@@ -30,6 +30,41 @@ def shard(n_items: int, rank: int, world: int) -> np.ndarray:
     return np.arange(rank, n_items, world, dtype=np.int64)
 
 
+def shard_bytes(n_total: int, world: int) -> int:
+    """Bytes of one rank's padded summary shard (ceil(n / world) records)."""
+    from ._abi import SUMMARY_DTYPE
+
+    return -(-n_total // world) * SUMMARY_DTYPE.itemsize
+
+
+def gather_summaries_into(local, padded, gathered) -> None:
+    """Device-side all-gather of the per-scenario summaries (the sweep's only
+    collective; NCCL over NVLink in bench.py, gloo in the CPU tests).
+
+    local     uint8 tensor, this rank's summaries (n_local records)
+    padded    uint8 tensor of shard_bytes(n_total, world) bytes (scratch)
+    gathered  uint8 tensor of world * shard_bytes(...) bytes (output)
+    """
+    import torch.distributed as dist
+
+    padded[: local.numel()].copy_(local)
+    dist.all_gather_into_tensor(gathered, padded)
+
+
+def assemble_gathered(gathered: np.ndarray, n_total: int, world: int) -> np.ndarray:
+    """Gathered shard bytes (rank-major) -> summaries in global scenario order
+    (inverse of the static interleave)."""
+    from ._abi import SUMMARY_DTYPE
+
+    per = shard_bytes(n_total, world)
+    raw = np.ascontiguousarray(gathered).view(np.uint8).reshape(world, per)
+    full = np.zeros(n_total, dtype=SUMMARY_DTYPE)
+    for r in range(world):
+        ids = shard(n_total, r, world)
+        full[ids] = raw[r, : len(ids) * SUMMARY_DTYPE.itemsize].view(SUMMARY_DTYPE)
+    return full
+
+
 def gather_summaries(local: np.ndarray, n_total: int, rank: int, world: int, device=None) -> np.ndarray:
     """All-gather every rank's shard of per-scenario summaries (the sweep's
     only collective) and return them in global scenario order.  Shards are

@@ -6,6 +6,13 @@ C2  request-rate sweep, 32 rates (2..33 req/s) x {Arrow, static PD
     (minimal-load 4/4), PD-colocated (slo-aware, flips off, 8/0)}, 8
     instances, bundled bursty trace (2 606 requests), the rate-sweep config
     of test_acceptance.py:55-72.
+C3  code-like / conversation-like traces x 8 rates (2..16 req/s) x the
+    TTFT x TPOT SLO grid (8 x 5) x 3 policies, 8 instances: 1 920 runs
+    (thresholds and the decode token cap derive from the SLO,
+    scheduler.py:75-81, cost_model.py:125-139).
+C4  pool-size x flip-threshold ablation: N in {16,24,32,48,64} x theta_d x
+    theta_busy x breach x ttft_threshold x 2 rates, Arrow, 10 000 requests:
+    1 080 runs.
 C5  mixed-radix scenario sweep: 4 traces x 32 per-instance rates x 3
     policies x N in {4,8,16,32} x theta_d x theta_busy x breach duration.
 
@@ -100,6 +107,76 @@ def code_like_trace():
 def conversation_like_trace():
     return gen_synthetic(SyntheticParams(600.0, 4.0, math.log(800), 0.8, math.log(250), 0.6,
                                          (BurstEpisode(120, 120, 1.5), BurstEpisode(360, 120, 2.0)), 8000, 2000, 202))
+
+
+C3_RATES = (2.0, 4.0, 6.0, 8.0, 10.0, 12.0, 14.0, 16.0)
+C3_TTFT = (0.25, 0.5, 1.0, 2.0, 3.0, 5.0, 10.0, 30.0)
+C3_TPOT = (0.025, 0.05, 0.075, 0.1, 0.15)
+
+
+def c3(ids=None) -> list[Scenario]:
+    """Scenario id -> (trace, rate, ttft slo, tpot slo, policy) in mixed radix
+    2 x 8 x 8 x 5 x 3 = 1 920."""
+    traces = [code_like_trace(), conversation_like_trace()]
+    natives = [native_rate(t) for t in traces]
+    base = default_run_config()
+    total = 2 * 8 * 8 * 5 * 3
+    out = []
+    cache: dict = {}
+    for sid in (range(total) if ids is None else ids):
+        x = int(sid)
+        tr, x = x % 2, x // 2
+        k, x = x % 8, x // 8
+        a, x = x % 8, x // 8
+        b, x = x % 5, x // 5
+        pol = x % 3
+        key = (a, b, pol)
+        cfg = cache.get(key)
+        if cfg is None:
+            slo = dataclasses.replace(base.slo, ttft_slo=C3_TTFT[a], tpot_slo=C3_TPOT[b])
+            cfg = cache[key] = policy_config(dataclasses.replace(base, slo=slo), POLICIES[pol], 8)
+        out.append(Scenario(traces[tr], cfg, natives[tr] / C3_RATES[k], sid))
+    return out
+
+
+def c4_trace():
+    return gen_synthetic(SyntheticParams(3600.0, 4.0, math.log(420), 0.55, math.log(130), 0.5,
+                                         (BurstEpisode(600, 120, 5), BurstEpisode(1800, 180, 4)), 3500, 900, 3))[:10000]
+
+
+C4_N = (16, 24, 32, 48, 64)
+C4_THETA_D = (0.25, 0.5, 0.75, 1.0)
+C4_THETA_BUSY = (0.5, 0.75, 0.9)
+C4_BREACH = (1.0, 2.0, 4.0)
+C4_TTFT_FACTOR = (0.5, 0.75, 1.0)
+C4_RATE_FACTOR = (1.25, 2.5)
+
+
+def c4(ids=None) -> list[Scenario]:
+    """Scenario id -> (N, theta_d, theta_busy, breach, ttft threshold, rate)
+    in mixed radix 5 x 4 x 3 x 3 x 3 x 2 = 1 080, Arrow."""
+    trace = c4_trace()
+    native = native_rate(trace)
+    base = default_run_config()
+    total = 5 * 4 * 3 * 3 * 3 * 2
+    out = []
+    for sid in (range(total) if ids is None else ids):
+        x = int(sid)
+        ni, x = x % 5, x // 5
+        td, x = x % 4, x // 4
+        tb, x = x % 3, x // 3
+        br, x = x % 3, x // 3
+        tf, x = x % 3, x // 3
+        rf = x % 2
+        n = C4_N[ni]
+        sched = dataclasses.replace(base.scheduler, theta_d=C4_THETA_D[td], theta_busy=C4_THETA_BUSY[tb],
+                                    tpot_breach_duration_s=C4_BREACH[br],
+                                    ttft_threshold=C4_TTFT_FACTOR[tf] * base.slo.ttft_slo)
+        cfg = policy_config(dataclasses.replace(base, scheduler=sched), "arrow", n)
+        cfg = dataclasses.replace(cfg, scheduler=dataclasses.replace(cfg.scheduler,
+                                                                     ttft_threshold=sched.ttft_threshold))
+        out.append(Scenario(trace, cfg, native / (C4_RATE_FACTOR[rf] * n), sid))
+    return out
 
 
 C5_THETA_D = (0.25, 0.5, 0.75, 1.0)

@@ -42,6 +42,8 @@ def oracle_lib() -> ctypes.CDLL:
         lib = ctypes.CDLL(str(path))
         lib.pdsim_oracle_run_batch.argtypes = [ctypes.c_void_p, ctypes.c_int]
         lib.pdsim_oracle_run_batch.restype = ctypes.c_int
+        lib.pdsim_oracle_run_batch_timed.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+        lib.pdsim_oracle_run_batch_timed.restype = ctypes.c_int
         lib.pdsim_oracle_pysum.argtypes = [ctypes.c_void_p, ctypes.c_int64]
         lib.pdsim_oracle_pysum.restype = ctypes.c_double
         lib.pdsim_oracle_decision_hash.argtypes = [ctypes.c_void_p, ctypes.c_int64]
@@ -111,6 +113,16 @@ def run_oracle(cb, spec=FULL, threads=1, tokens=False) -> HostBuffers:
     b = hb.host_struct()
     oracle_lib().pdsim_oracle_run_batch(ctypes.addressof(b), threads)
     return hb
+
+
+def run_oracle_timed(cb, threads=0):
+    """Summaries of the CPU port plus each scenario's wall seconds on its
+    worker thread (bench.py's CPU baseline)."""
+    hb = HostBuffers(cb, OutputSpec())
+    b = hb.host_struct()
+    secs = np.zeros(cb.n, dtype=np.float64)
+    used = oracle_lib().pdsim_oracle_run_batch_timed(ctypes.addressof(b), threads, secs.ctypes.data)
+    return hb, secs, used
 
 
 def run_emu(cb, spec=FULL, width=8, variant: str = "") -> HostBuffers:

@@ -1,0 +1,81 @@
+"""BASELINE sweeps on the B200 against the CPU oracle (needs a GPU).
+
+The oracle is pinned to the real reference on the C3/C4/C5 golden fixtures
+(test_oracle_golden.py); here the CUDA evaluator runs seeded samples of the
+full C3, C4 and C5 sweeps (workloads.py, the exact scenarios bench.py
+times) and every per-scenario summary field, the decision-stream digest and
+every request's first/last token time and dispatch targets must equal the
+oracle's bit for bit, stalled scenarios included."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import harness as H
+from paper_2505_11916_b200 import _abi, engine
+from paper_2505_11916_b200 import workloads as W
+from paper_2505_11916_b200._buffers import OutputSpec
+from paper_2505_11916_b200._compile import compile_batch, dispatch_order
+
+pytestmark = pytest.mark.gpu
+
+SUMMARY_INT = ("status", "n_completed", "n_ok", "n_flips", "n_events", "n_iterations", "n_decisions", "n_ticks",
+               "decision_hash")
+SUMMARY_F64 = ("stall_time", "attainment", "p90_ttft", "p90_tpot", "mean_ttft", "mean_tpot", "goodput", "span")
+
+
+@pytest.fixture(scope="module")
+def evaluator():
+    from paper_2505_11916_b200._backend import CudaEvaluator
+
+    return CudaEvaluator()
+
+
+def _compare(got, exp, n):
+    for f in SUMMARY_INT:
+        g, e = got.summaries[f], exp.summaries[f]
+        bad = np.nonzero(g != e)[0]
+        assert bad.size == 0, f"{f}: {bad.size} scenarios differ, first {bad[0]}: {g[bad[0]]} vs {e[bad[0]]}"
+    for f in SUMMARY_F64:
+        H.assert_same_f64(got.summaries[f], exp.summaries[f], f)
+    H.assert_same_f64(got.req_first, exp.req_first, "first")
+    np.testing.assert_array_equal(got.req_prefill, exp.req_prefill)
+    np.testing.assert_array_equal(got.req_decode, exp.req_decode)
+    for s in range(n):
+        if int(exp.summaries[s]["status"]) == _abi.OK:   # stalled runs raise; partial records unobserved
+            sl = got.req_slice(s)
+            H.assert_same_f64(got.req_last[sl], exp.req_last[sl], f"scenario {s} last")
+
+
+def _run(evaluator, scenarios):
+    cb = compile_batch(scenarios, engine.STALL_EVENT_LIMIT)
+    spec = OutputSpec(requests=True)
+    got = evaluator.execute(cb, spec, dispatch_order(cb))
+    exp = H.run_oracle(cb, spec, threads=0)
+    _compare(got, exp, cb.n)
+    return got
+
+
+def test_c5_sample_of_2048_matches_oracle(evaluator):
+    """2 048 seeded C5 scenario ids (all traces, rates, policies, N up to 32,
+    threshold axes), occupancy build (multi-wave), 500 000-event watchdog."""
+    ids = np.sort(np.random.default_rng(2048).choice(98304, size=2048, replace=False))
+    got = _run(evaluator, W.c5(ids))
+    assert (got.summaries["status"] == _abi.OK).sum() > 2000
+
+
+def test_c4_sample_matches_oracle(evaluator):
+    """C4: 10 000-request Arrow runs on 16-64 instances (two instances per lane
+    above 32), threshold ablation axes."""
+    ids = np.sort(np.random.default_rng(4).choice(1080, size=96, replace=False))
+    scs = W.c4(ids)
+    assert max(s.config.instance_count for s in scs) == 64
+    _run(evaluator, scs)
+
+
+def test_c3_sample_matches_oracle(evaluator):
+    """C3: code- and conversation-like traces over the TTFT x TPOT SLO grid
+    (Arrow re-simulated per SLO point: thresholds and token cap follow)."""
+    ids = np.sort(np.random.default_rng(3).choice(1920, size=192, replace=False))
+    _run(evaluator, W.c3(ids))

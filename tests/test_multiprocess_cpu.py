@@ -18,7 +18,7 @@ import torch.multiprocessing as mp
 import harness as H
 from paper_2505_11916_b200 import _abi
 from paper_2505_11916_b200._buffers import OutputSpec
-from paper_2505_11916_b200.sweep import gather_summaries, shard
+from paper_2505_11916_b200.sweep import assemble_gathered, gather_summaries, gather_summaries_into, shard, shard_bytes
 
 NAMES = ["small_arrow_2_2", "small_noflip", "rr_small", "fuzz_01", "fuzz_02", "fuzz_07", "fuzz_11"]
 
@@ -45,8 +45,15 @@ def _worker(rank, world, port, q):
     cb = compile_batch([H.golden_scenario(*items[i]) for i in mine], limit)
     hb = H.run_oracle(cb, OutputSpec(), threads=1)
     full = gather_summaries(hb.summaries, len(items), rank, world)
+    # the exact device-side path of bench.py (all_gather_into_tensor of
+    # padded byte shards, then assembly in global order)
+    local = torch.from_numpy(np.ascontiguousarray(hb.summaries).view(np.uint8).reshape(-1).copy())
+    padded = torch.zeros(shard_bytes(len(items), world), dtype=torch.uint8)
+    gathered = torch.empty(world * padded.numel(), dtype=torch.uint8)
+    gather_summaries_into(local, padded, gathered)
+    full2 = assemble_gathered(gathered.numpy(), len(items), world)
     if rank == 0:
-        q.put(full.tobytes())
+        q.put((full.tobytes(), full2.tobytes()))
     dist.destroy_process_group()
 
 
@@ -58,7 +65,7 @@ def test_sharded_sweep_gathers_to_single_process_result():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    data = q.get(timeout=300)
+    data, data2 = q.get(timeout=300)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -69,6 +76,7 @@ def test_sharded_sweep_gathers_to_single_process_result():
     cb = compile_batch([H.golden_scenario(m, a) for m, a in items], items[0][0]["stall_limit"])
     ref = H.run_oracle(cb, OutputSpec(), threads=1).summaries
     assert gathered.tobytes() == ref.tobytes()
+    assert data2 == ref.tobytes()            # bench.py's all_gather_into_tensor path
     for s, (m, a) in enumerate(items):
         assert H.bits(gathered[s]["attainment"]) == H.bits(m["summary"]["attainment"])
 
