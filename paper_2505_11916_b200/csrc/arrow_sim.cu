@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) arrow_sim_kernel(const arrow_b
   const int wid = threadIdx.x >> 5;
   const int slot = blockIdx.x * WPB + wid;
   if (slot >= n_slots) return;
-  arrow::Sim<DevWarp, IPL> sim;
+  arrow::Sim<DevWarp, IPL, (MINB > 1)> sim;   // occupancy build: COMPACT code
   sim.sm = &smem[wid];
   sim.B = &sb;
   sim.L = L;

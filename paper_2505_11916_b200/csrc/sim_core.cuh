@@ -303,7 +303,12 @@ AS_HD int imin(int a, int b) { return a < b ? a : b; }
   } while (0)
 #endif
 
-template <class W, int IPL>
+// COMPACT (the occupancy build): code size over instruction count.  With 12
+// warps per SM at unrelated points of the event loop the hot code does not
+// fit the instruction caches (C5 ncu: 78 % of stall samples "no
+// instruction"), so repeated call sites are folded into non-unrolled loops.
+// The latency build (1-2 warps per SM) keeps them unrolled.
+template <class W, int IPL, bool COMPACT = false>
 struct Sim {
   W w;
   WarpSmem* sm;
@@ -765,7 +770,8 @@ struct Sim {
   // instance's state and per-request outputs, except (SERIAL only) the
   // PREFILL_COMPLETE FIFO and the push sequence.  Adds finished requests to
   // `completed`; returns the drained-pool move (-1 none); sets `pushed` when
-  // the next iteration started (its sequence is assigned here if SERIAL).
+  // the next iteration started (non-SERIAL: lane-parallel rounds; the serial
+  // path starts migrations and kicks in serial_tail()).
   template <bool SERIAL>
   AS_HD int iteration_complete(Inst& I, double now, int& completed, bool& pushed) {
     const int cur = I.it - 1;
@@ -854,10 +860,7 @@ struct Sim {
     else if (pk == P_D2P && !has_decode_work(I))
       dst = P_PREFILL;
     if (SERIAL) {
-      if (nd + npf > 0) u().esp = 0;
-      if (start_mig(I, now)) I.mig_seq = next_seq();
-      pushed = kick(I, now);
-      if (pushed) I.iter_seq = next_seq();
+      if (nd + npf > 0) u().esp = 0;   // _start_migrations + _kick follow in serial_tail()
     } else {
       pushed = kick(I, now);
     }
@@ -1128,57 +1131,52 @@ struct Sim {
     return w.shfl(id, ffs32(b));
   }
 
+  // schedule_prefill / schedule_decode log one dispatch at a single code site
+  // each; the choose_* bodies return (target | branch << 16), or -1.  The
+  // t1 / t2 candidate tests run in one non-unrolled loop (one inlined copy of
+  // the argmin and of the admission test instead of one per pool).
+  static AS_HD int pack_choice(int t, int branch) { return (t & 0xffff) | (branch << 16); }   // >= 0
+  static AS_HD int choice_target(int c) { return (int)(int16_t)(c & 0xffff); }
+
   // schedule_prefill, scheduler.py:151-195
   AS_HD int schedule_prefill(int rid, double now, double own) {
-    const int K = ARROW_DEC_PREFILL_DISPATCH;
+    const int c = choose_prefill(now, own);
+    if (c < 0) return -1;                // no instance (status set)
+    log_dispatch(now, ARROW_DEC_PREFILL_DISPATCH, rid, choice_target(c), c >> 16);
+    return choice_target(c);
+  }
+
+  AS_HD int choose_prefill(double now, double own) {
     const int strat = sc().strategy;
     if (strat == ARROW_STRATEGY_ROUND_ROBIN) {
       int chosen = rr_pick(P_PREFILL, u().rr_p);
       w.sync();
       lane0([&] { u().rr_p++; });
-      log_dispatch(now, K, rid, chosen, ARROW_BR_ROUND_ROBIN);
-      return chosen;
+      return pack_choice(chosen, ARROW_BR_ROUND_ROBIN);
     }
     compute_delays(now);
-    if (strat == ARROW_STRATEGY_MINIMAL_LOAD) {
-      int chosen = argmin_delay_pool(P_PREFILL);
-      log_dispatch(now, K, rid, chosen, ARROW_BR_MIN_LOAD);
-      return chosen;
-    }
+    if (strat == ARROW_STRATEGY_MINIMAL_LOAD) return pack_choice(argmin_delay_pool(P_PREFILL), ARROW_BR_MIN_LOAD);
     const double thr = sc().ttft_thr;
-    int t1 = argmin_delay_pool(P_PREFILL);
-    if (t1 >= 0 && delay_within(t1, own, thr)) {
-      log_dispatch(now, K, rid, t1, ARROW_BR_ALG1_T1);
-      return t1;
-    }
-    int t2 = argmin_delay_pool(P_D2P);
-    if (t2 >= 0 && delay_within(t2, own, thr)) {
-      log_dispatch(now, K, rid, t2, ARROW_BR_ALG1_T2);
-      return t2;
+    int t1 = -1, t2 = -1;
+#pragma unroll 1
+    for (int c = 0; c < 2; c++) {       // t1 over PREFILL, then t2 over D_TO_P (scheduler.py:168-175)
+      const int t = argmin_delay_pool(c == 0 ? P_PREFILL : P_D2P);
+      if (c == 0) t1 = t; else t2 = t;
+      if (t >= 0 && delay_within(t, own, thr)) return pack_choice(t, c == 0 ? ARROW_BR_ALG1_T1 : ARROW_BR_ALG1_T2);
     }
     if (sc().enable_flips && decode_load_is_low(now)) {
       int t3 = try_move_d2p(now, ARROW_TRIG_ALG1);
-      if (t3 >= 0) {
-        log_dispatch(now, K, rid, t3, ARROW_BR_ALG1_FLIP);
-        return t3;
-      }
+      if (t3 >= 0) return pack_choice(t3, ARROW_BR_ALG1_FLIP);
     }
-    if (t1 >= 0) {
-      log_dispatch(now, K, rid, t1, ARROW_BR_ALG1_FALLBACK);
-      return t1;
-    }
-    if (t2 >= 0) {
-      log_dispatch(now, K, rid, t2, ARROW_BR_ALG1_FALLBACK);
-      return t2;
-    }
+    if (t1 >= 0) return pack_choice(t1, ARROW_BR_ALG1_FALLBACK);
+    if (t2 >= 0) return pack_choice(t2, ARROW_BR_ALG1_FALLBACK);
     int chosen = argmin_delay([&](const Inst& I) { return decode_role(I.id); },
                               [&](const Inst& I) { return (uint32_t)decode_role_tie(I.id); });
     if (chosen < 0) {
       lane0([&] { set_status(ARROW_NO_INSTANCE); });
       return -1;
     }
-    log_dispatch(now, K, rid, chosen, ARROW_BR_ALG1_DEGENERATE);
-    return chosen;
+    return pack_choice(chosen, ARROW_BR_ALG1_DEGENERATE);
   }
 
   // _decode_admissible, scheduler.py:214-218
@@ -1197,59 +1195,49 @@ struct Sim {
 
   // schedule_decode, scheduler.py:199-254
   AS_HD int schedule_decode(int rid, int src, double now) {
-    const int K = ARROW_DEC_DECODE_DISPATCH;
+    const int c = choose_decode(src, now);
+    log_dispatch(now, ARROW_DEC_DECODE_DISPATCH, rid, choice_target(c), c >> 16);
+    return choice_target(c);
+  }
+
+  AS_HD int choose_decode(int src, double now) {
     const int strat = sc().strategy;
     if (strat == ARROW_STRATEGY_ROUND_ROBIN) {
       int chosen = rr_pick(P_DECODE, u().rr_d);
       w.sync();
       lane0([&] { u().rr_d++; });
-      log_dispatch(now, K, rid, chosen, ARROW_BR_ROUND_ROBIN);
-      return chosen;
+      return pack_choice(chosen, ARROW_BR_ROUND_ROBIN);
     }
-    if (strat == ARROW_STRATEGY_MINIMAL_LOAD) {
-      int chosen = argmin_tokens_pool(P_DECODE);
-      log_dispatch(now, K, rid, chosen, ARROW_BR_MIN_LOAD);
-      return chosen;
-    }
-    if (decode_role(src)) {
-      log_dispatch(now, K, rid, src, ARROW_BR_ALG2_ZERO_TRANSFER);
-      return src;
-    }
-    int t1 = argmin_tokens_pool(P_DECODE);
-    int tok1 = t1 >= 0 ? bcast_i(t1, [](Inst& I) { return I.rtok; }) : 0;
-    if (t1 >= 0 && decode_admissible(t1, tok1, now)) {
-      log_dispatch(now, K, rid, t1, ARROW_BR_ALG2_T1);
-      return t1;
-    }
-    int t2 = argmin_tokens_pool(P_P2D);
-    int tok2 = t2 >= 0 ? bcast_i(t2, [](Inst& I) { return I.rtok; }) : 0;
-    if (t2 >= 0 && decode_admissible(t2, tok2, now)) {
-      log_dispatch(now, K, rid, t2, ARROW_BR_ALG2_T2);
-      return t2;
+    if (strat == ARROW_STRATEGY_MINIMAL_LOAD) return pack_choice(argmin_tokens_pool(P_DECODE), ARROW_BR_MIN_LOAD);
+    if (decode_role(src)) return pack_choice(src, ARROW_BR_ALG2_ZERO_TRANSFER);
+    int t1 = -1, t2 = -1, tok1 = 0, tok2 = 0;
+#pragma unroll 1
+    for (int c = 0; c < 2; c++) {       // t1 over DECODE, then t2 over P_TO_D (scheduler.py:225-234)
+      const int t = argmin_tokens_pool(c == 0 ? P_DECODE : P_P2D);
+      const int tok = t >= 0 ? bcast_i(t, [](Inst& I) { return I.rtok; }) : 0;
+      if (c == 0) {
+        t1 = t;
+        tok1 = tok;
+      } else {
+        t2 = t;
+        tok2 = tok;
+      }
+      if (t >= 0 && decode_admissible(t, tok, now)) return pack_choice(t, c == 0 ? ARROW_BR_ALG2_T1 : ARROW_BR_ALG2_T2);
     }
     if (sc().enable_flips) {
       compute_delays(now);
       int t3 = try_move_p2d(now, ARROW_TRIG_ALG2);
-      if (t3 >= 0) {
-        log_dispatch(now, K, rid, t3, ARROW_BR_ALG2_FLIP);
-        return t3;
-      }
+      if (t3 >= 0) return pack_choice(t3, ARROW_BR_ALG2_FLIP);
     }
-    if (t1 >= 0 && (t2 < 0 || tok1 <= tok2)) {
-      log_dispatch(now, K, rid, t1, ARROW_BR_ALG2_FALLBACK);
-      return t1;
-    }
-    if (t2 >= 0) {
-      log_dispatch(now, K, rid, t2, ARROW_BR_ALG2_FALLBACK);
-      return t2;
-    }
-    log_dispatch(now, K, rid, src, ARROW_BR_ALG2_FORCED_LOCAL);
-    return src;
+    if (t1 >= 0 && (t2 < 0 || tok1 <= tok2)) return pack_choice(t1, ARROW_BR_ALG2_FALLBACK);
+    if (t2 >= 0) return pack_choice(t2, ARROW_BR_ALG2_FALLBACK);
+    return pack_choice(src, ARROW_BR_ALG2_FORCED_LOCAL);
   }
 
   // ------------------------------------------------------- handlers ----
 
-  AS_HD void on_arrival(double now) {
+  // returns the instance to kick (serial_tail), -1 if none
+  AS_HD int on_arrival(double now) {
     const int rid = u().a;
     const double own = quad(sc().pred_a2, sc().pred_a1, sc().pred_a0, inl[rid]);
     w.sync();
@@ -1259,7 +1247,7 @@ struct Sim {
       U.next_arrival = U.a < sc().n_requests ? arr[U.a] * sc().arrival_scale : 0.0;
     });
     int target = schedule_prefill(rid, now, own);
-    if (target < 0) return;
+    if (target < 0) return -1;
     owner(target, [&](Inst& I) {
       if (I.wp_c >= L.qcap) {
         set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_QUEUE);
@@ -1271,11 +1259,12 @@ struct Sim {
       I.wp_c++;
       dd_add(I.ws_hi, I.ws_lo, own);
       if (fabs(own) > I.ws_max) I.ws_max = fabs(own);
-      if (kick(I, now)) I.iter_seq = next_seq();
     });
+    return target;
   }
 
-  AS_HD void on_prefill_complete(double now) {
+  // returns the decode target; *mig: a migration may start on it (serial_tail)
+  AS_HD int on_prefill_complete(double now, bool* mig) {
     int rid = 0, src = 0;
     {
       Uniform& U = u();
@@ -1302,8 +1291,6 @@ struct Sim {
         mq_rid(I.id)[ring(I.mq_h, I.mq_c, L.qcap)] = rid;
         if (I.mq_c == 0) I.mq_need = inl[rid] + (outl[rid] - 1);
         I.mq_c++;
-        if (start_mig(I, now)) I.mig_seq = next_seq();
-        if (kick(I, now)) I.iter_seq = next_seq();
         return;
       }
       if (I.wd_c >= L.qcap) {
@@ -1314,11 +1301,12 @@ struct Sim {
       I.wd_c++;
       I.wgrowth += g;
       I.rtok += in;
-      if (kick(I, now)) I.iter_seq = next_seq();
     });
+    *mig = target != src;
+    return target;
   }
 
-  AS_HD void on_migration_complete(int id, double now) {
+  AS_HD int on_migration_complete(int id, double now) {
     owner(id, [&](Inst& I) {
       int rid = I.mig_rid;
       I.mig_active = 0;
@@ -1342,18 +1330,34 @@ struct Sim {
       S.kv_used -= inl[rid];   // release_parked
       S.parked--;
     });
-    owner(id, [&](Inst& I) {
-      if (start_mig(I, now)) I.mig_seq = next_seq();
-    });
-    owner(src, [&](Inst& S) {
-      if (start_mig(S, now)) S.mig_seq = next_seq();
-    });
-    owner(id, [&](Inst& I) {
-      if (kick(I, now)) I.iter_seq = next_seq();
-    });
-    owner(src, [&](Inst& S) {
-      if (kick(S, now)) S.iter_seq = next_seq();
-    });
+    return src;                // serial_tail: migrations (id, src), then kicks (id, src)
+  }
+
+  // The serial handlers' trailing _start_migrations / _kick calls in program
+  // order (engine.py:211-223, 228-236, 240-248), from one code site: each
+  // inlined copy of kick() is ~300 instructions, and the occupancy build's
+  // hot loop does not fit the instruction cache as it is.
+  AS_HD void serial_tail(int m0, int m1, int k0, int k1, double now) {
+    if (u().status != ARROW_OK) return;
+    auto step = [&](int q) {
+      const int id = q == 0 ? m0 : q == 1 ? m1 : q == 2 ? k0 : k1;
+      if (id < 0) return;
+      const bool mig = q < 2;
+      owner(id, [&](Inst& I) {
+        if (mig) {
+          if (start_mig(I, now)) I.mig_seq = next_seq();
+        } else if (kick(I, now)) {
+          I.iter_seq = next_seq();
+        }
+      });
+    };
+    if constexpr (COMPACT) {
+#pragma unroll 1
+      for (int q = 0; q < 4; q++) step(q);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; q++) step(q);
+    }
   }
 
   AS_HD void write_snapshots(double now) {
@@ -2320,12 +2324,15 @@ struct Sim {
 #ifdef ARROW_PROF
       const int prof_kind = ev >= 1000 ? ev - 1000 : ((ev & 1) ? 5 : 6);
 #endif
+      int tm0 = -1, tm1 = -1, tk0 = -1, tk1 = -1;   // serial_tail() arguments
       if (ev >= 1000) {
         int kind = ev - 1000;
         if (kind == EV_ARRIVAL) {
-          on_arrival(now);
+          tk0 = on_arrival(now);
         } else if (kind == EV_PREFILL) {
-          on_prefill_complete(now);
+          bool mig = false;
+          tk0 = on_prefill_complete(now, &mig);
+          if (mig) tm0 = tk0;
         } else {
           lane0([&] { u().n_ticks++; });
           write_snapshots(now);
@@ -2376,10 +2383,14 @@ struct Sim {
           dst = u().tmp_i[0];
           w.sync();
           if (dst >= 0) move_and_log(id, dst, now, ARROW_TRIG_DRAINED);
+          tm0 = tk0 = id;
         } else {
-          on_migration_complete(id, now);
+          const int src = on_migration_complete(id, now);
+          tm0 = tk0 = id;
+          tm1 = tk1 = src;
         }
       }
+      serial_tail(tm0, tm1, tk0, tk1, now);
       const int status = u().status;
       const int64_t esp = u().esp;
       w.sync();
