@@ -63,6 +63,12 @@ def check_device_limits(config: RunConfig) -> None:
         raise ValueError(f"the device evaluator supports up to {MAX_INSTANCES} instances, got {config.instance_count}")
     if config.instance.kv_capacity_tokens > KV_LIMIT:
         raise ValueError(f"kv_capacity_tokens above {KV_LIMIT} is not supported by the device evaluator")
+    if config.instance.chunk_budget > KV_LIMIT:
+        raise ValueError(f"chunk_budget above {KV_LIMIT} is not supported by the device evaluator")
+    # transfer_time (cost_model.py:88-92) multiplies prompt_len * bytes_per_token
+    # as an exact Python int; the device uses int64 (prompt_len <= kv capacity)
+    if config.instance.kv_capacity_tokens * config.instance.transfer.bytes_per_token >= 1 << 63:
+        raise ValueError("kv_capacity_tokens * bytes_per_token must stay below 2**63 for the device evaluator")
 
 
 def min_iteration(config: RunConfig) -> float:
@@ -282,7 +288,9 @@ def scenario_record(config: RunConfig, trace_offset: int, n: int, scale: float, 
     rec["enable_flips"] = 1 if sched.enable_flips else 0
     rec["kv_capacity"] = inst.kv_capacity_tokens
     rec["chunk_budget"] = inst.chunk_budget
-    rec["max_batch"] = inst.max_batch_requests
+    # only min(max_batch_requests, chunk_budget) is ever used (instance.py:183);
+    # the reference accepts e.g. 10**10 as "unbounded"
+    rec["max_batch"] = min(inst.max_batch_requests, inst.chunk_budget)
     rec["bytes_per_token"] = inst.transfer.bytes_per_token
     rec["max_tokens"] = max_tokens
     rec["stall_limit"] = stall_limit

@@ -73,15 +73,22 @@ def execute(scenarios: list[Scenario], spec: OutputSpec, evaluator=None, order=N
         spec = OutputSpec(**grown)
 
 
-def run(trace: list[TraceRequest], config: RunConfig) -> RunResult:
-    """Simulate a trace under a configuration; deterministic for fixed inputs."""
-    cb, hb = execute([Scenario(trace, config, 1.0)], FULL_OUTPUTS)
-    _results.raise_for_status(hb, 0)
-    entry = cb.table.entries[0]
-    decisions = _results.decision_dicts(hb, 0, entry.ids)
+def result_from_buffers(cb, hb, s: int, config: RunConfig) -> RunResult:
+    """The reference's RunResult (engine.py:86-91) for scenario s of a launch
+    with FULL_OUTPUTS; raises the reference's exception for a failed run."""
+    _results.raise_for_status(hb, s)
+    entry = cb.table.entries[cb.trace_index[s]]
+    decisions = _results.decision_dicts(hb, s, entry.ids)
     return RunResult(
-        records=_results.records(hb, 0, entry.arrival, entry.ids, config.slo),
-        snapshots=_results.snapshots(hb, 0),
+        records=_results.records(hb, s, entry.arrival * float(cb.scenarios["arrival_scale"][s]), entry.ids,
+                                 config.slo),
+        snapshots=_results.snapshots(hb, s),
         decisions=decisions,
         transitions=_results.transitions(decisions),
     )
+
+
+def run(trace: list[TraceRequest], config: RunConfig) -> RunResult:
+    """Simulate a trace under a configuration; deterministic for fixed inputs."""
+    cb, hb = execute([Scenario(trace, config, 1.0)], FULL_OUTPUTS)
+    return result_from_buffers(cb, hb, 0, config)

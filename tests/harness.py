@@ -248,3 +248,19 @@ def assert_same_run(got, exp, n: int) -> None:
             assert_same_f64(got.req_last[sl], exp.req_last[sl], f"scenario {s} last")
     np.testing.assert_array_equal(got.req_prefill, exp.req_prefill)
     np.testing.assert_array_equal(got.req_decode, exp.req_decode)
+
+
+class OracleEvaluator:
+    """The CPU oracle behind the CudaEvaluator interface (.execute), so tests
+    can drive the package's host-side paths (result assembly, writers, CLI)
+    on a machine without a GPU.  Test-only: the product has no CPU path."""
+
+    def execute(self, cb, spec, order=None):
+        return run_oracle(cb, spec)
+
+
+def use_oracle_backend(monkeypatch) -> None:
+    from paper_2505_11916_b200 import _backend
+
+    ev = OracleEvaluator()
+    monkeypatch.setattr(_backend, "default_evaluator", lambda: ev)

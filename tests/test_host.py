@@ -163,3 +163,25 @@ def test_output_writers_round_trip(tmp_path):
     assert [r["ttft_s"] for r in rows] == [r.ttft for r in recs]
     assert paths["decisions"].read_text().count("\n") == len(dec)
     assert math.isfinite(float(paths["summary"].read_text().split('"attainment": ')[1].split(",")[0]))
+
+
+def test_unbounded_max_batch_and_transfer_product_limits():
+    """max_batch_requests above int32 (the reference accepts e.g. 10**10 as
+    unbounded) compiles to min(max_batch, chunk_budget), the only value the
+    batch former uses (instance.py:183); a prompt * bytes_per_token product
+    that could overflow int64 on the device is rejected up front."""
+    import dataclasses
+
+    from paper_2505_11916_b200._compile import Scenario, compile_batch
+    from paper_2505_11916_b200.config import default_run_config
+    from paper_2505_11916_b200.core import TraceRequest
+
+    base = default_run_config()
+    trace = [TraceRequest(0, 0.0, 100, 5), TraceRequest(1, 1.0, 100, 5)]
+    cfg = dataclasses.replace(base, instance=dataclasses.replace(base.instance, max_batch_requests=10**10))
+    cb = compile_batch([Scenario(trace, cfg, 1.0)], 500_000)
+    assert int(cb.scenarios["max_batch"][0]) == base.instance.chunk_budget
+    big = dataclasses.replace(base.instance.transfer, bytes_per_token=1 << 50)
+    cfg = dataclasses.replace(base, instance=dataclasses.replace(base.instance, transfer=big))
+    with pytest.raises(ValueError, match="bytes_per_token"):
+        compile_batch([Scenario(trace, cfg, 1.0)], 500_000)
