@@ -9,6 +9,7 @@ PKG := paper_2505_11916_b200
 CSRC := $(PKG)/csrc
 LIBDIR := $(PKG)/lib
 LIB := $(LIBDIR)/libarrow_sim.so
+AUDIT_LIB := $(LIBDIR)/libarrow_sim_audit.so
 HDRS := include/arrow_sim.h include/arrow_traces.h $(CSRC)/sim_core.cuh $(CSRC)/warp.cuh \
 	$(CSRC)/npgen.cuh $(CSRC)/npgen_tables.h
 SRCS := $(CSRC)/arrow_sim.cu $(CSRC)/traces.cu $(CSRC)/stats.cu
@@ -17,16 +18,22 @@ NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -fmad=false -prec-div=true -Xptxas -
 
 all: lib oracle emu
 
-lib: $(LIB)
+lib: $(LIB) $(AUDIT_LIB)
 
 $(LIB): $(SRCS) $(HDRS)
 	@mkdir -p $(LIBDIR)
 	$(NVCC) $(NVFLAGS) -o $@ $(SRCS) 2> $(LIBDIR)/ptxas.log || (cat $(LIBDIR)/ptxas.log; exit 1)
 
+# RunConfig.audit=True: per-step KV / pool-partition checks (engine.py:279-282)
+$(AUDIT_LIB): $(SRCS) $(HDRS)
+	@mkdir -p $(LIBDIR)
+	$(NVCC) $(NVFLAGS) -DARROW_AUDIT -o $@ $(SRCS) 2> $(LIBDIR)/ptxas_audit.log || (cat $(LIBDIR)/ptxas_audit.log; exit 1)
+
 oracle:
 	$(MAKE) -s -C oracle
 
-emu: build/libarrow_emu.so build/libarrow_emu_wide.so build/libarrow_emu_mut.so build/libnpgen_host.so
+emu: build/libarrow_emu.so build/libarrow_emu_wide.so build/libarrow_emu_mut.so build/libarrow_emu_audit.so \
+	build/libnpgen_host.so
 
 build/libarrow_emu.so: $(CSRC)/emu/emu.cpp $(HDRS)
 	@mkdir -p build
@@ -40,12 +47,18 @@ build/libarrow_emu_wide.so: $(CSRC)/emu/emu.cpp $(HDRS)
 	$(CXX_HOST) -std=c++20 -O2 -g -fPIC -shared -ffp-contract=off -fno-fast-math -pthread \
 		-Wall -Wno-unknown-pragmas -DARROW_DELAY_SLACK=0x1p-12 -Iinclude -o $@ $(CSRC)/emu/emu.cpp
 
-# test-only mutant: the burst merge's equal-time fallback in reversed order
-# (tests prove the tie fixture can tell it from the shipped source)
+# test-only mutants (ARROW_MUTANT=tie|kv at run time) with the audit checks:
+# tests prove the tie fixture and the audit build catch them
 build/libarrow_emu_mut.so: $(CSRC)/emu/emu.cpp $(HDRS)
 	@mkdir -p build
 	$(CXX_HOST) -std=c++20 -O2 -g -fPIC -shared -ffp-contract=off -fno-fast-math -pthread \
-		-Wall -Wno-unknown-pragmas -DARROW_MUTATE_TIE_REVERSE -Iinclude -o $@ $(CSRC)/emu/emu.cpp
+		-Wall -Wno-unknown-pragmas -DARROW_MUTANTS -DARROW_AUDIT -Iinclude -o $@ $(CSRC)/emu/emu.cpp
+
+# the audit build's checks, run by the emulator on CPU
+build/libarrow_emu_audit.so: $(CSRC)/emu/emu.cpp $(HDRS)
+	@mkdir -p build
+	$(CXX_HOST) -std=c++20 -O2 -g -fPIC -shared -ffp-contract=off -fno-fast-math -pthread \
+		-Wall -Wno-unknown-pragmas -DARROW_AUDIT -Iinclude -o $@ $(CSRC)/emu/emu.cpp
 
 build/libnpgen_host.so: $(CSRC)/emu/npgen_host.cpp $(HDRS)
 	@mkdir -p build

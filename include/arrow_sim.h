@@ -96,7 +96,8 @@ enum arrow_status {
   ARROW_NO_INSTANCE = 4,      /* RuntimeError, scheduler.py:192-193 */
   ARROW_ZERO_DIVISION = 5,    /* aggregate / capacity with max_tokens == 0, scheduler.py:322 */
   ARROW_BUFFER_OVERFLOW = 6,  /* a caller-sized buffer or ring was too small; re-run larger */
-  ARROW_INTERNAL = 7          /* an invariant the reference raises on was violated */
+  ARROW_INTERNAL = 7,         /* an invariant the reference raises on was violated */
+  ARROW_AUDIT_FAILED = 8      /* audit build: per-step KV / partition check failed (engine.py:279-282) */
 };
 
 /* which buffer overflowed (arrow_summary_t.overflow) */

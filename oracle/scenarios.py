@@ -331,25 +331,23 @@ def c5_scenario(make, sid, traces=None):
     return trace, v, rate_scale(trace, rate)
 
 
-def tie_flip_trace(make):
-    """Burst-merge tie case.  Two decode instances (2 and 3) receive identical
-    decode work at the same instant, so their decode-only iteration chains run
-    in lockstep and end a burst with pending completions at exactly the same
-    time (the burst merge's equal-time fallback assigns their sequence
-    numbers).  Two long prompts then arrive while both prefill instances are
-    busy: Alg. 1 flips decode instances 2 and 3 into D_TO_P, and when their
-    tied completions drain them the two `drained` flips are logged in (time,
-    kind, seq) order -- so the order of the tied sequence numbers is visible in
-    the decision stream and in the PREFILL pool's insertion order."""
-    reqs = []
-    for j in range(4):                      # identical short requests -> identical decode work on 2 and 3
-        reqs.append((0.0, 40, 60))
-    for j in range(6):                      # long prompts: prefill instances saturate, Alg. 1 flips decodes
-        reqs.append((0.5 + 0.01 * j, 3000, 2))
-    for j in range(6):                      # later arrivals dispatched over the re-grown PREFILL pool
-        reqs.append((3.0 + 0.05 * j, 200, 3))
-    reqs.sort(key=lambda r: r[0])
+def tie_lockstep_trace(make, t_arrive):
+    """Burst-merge tie case.  Two PD-colocated instances get identical
+    requests at t=0 and decode them in lockstep: their decode-only iteration
+    chains run as chain bursts whose final pending completions fall at exactly
+    the same time, so the burst merge's equal-time fallback assigns their
+    sequence numbers.  Two identical short prompts arriving at t_arrive (one
+    per instance) join those instances' next batches; both prefills finish
+    in the same iteration on both instances, and the two PREFILL_COMPLETE
+    events -- and so the two decode_dispatch records -- come out in the order
+    of the tied sequence numbers.  A merge that reversed equal-time finals
+    logs request 3 before request 2 (tests/test_emulated_kernel.py runs that
+    mutant)."""
+    reqs = [(0.0, 100, 200), (0.0, 100, 200), (t_arrive, 50, 5), (t_arrive, 50, 5)]
     return [make(i, a, il, ol) for i, (a, il, ol) in enumerate(reqs)]
+
+
+TIE_ARRIVALS = (0.503, 0.52, 0.53, 0.71, 0.8)
 
 
 def catalogue_r2(make, c5_count=32, which=("c3", "c4", "c5", "tie")):
@@ -376,6 +374,7 @@ def catalogue_r2(make, c5_count=32, which=("c3", "c4", "c5", "tie")):
             tr, v, sc = c5_scenario(make, sid, traces)
             add(f"c5_{sid:05d}", tr, v, scale=sc)
     if "tie" in which:
-        v = cfg(instances=4, init_prefill=2, init_decode=2, **ENGINE_TEST)
-        add("tie_drained_flips", tie_flip_trace(make), v, full=True)
+        v = cfg(instances=2, init_prefill=2, init_decode=0, enable_flips=False, **ENGINE_TEST)
+        for t in TIE_ARRIVALS:
+            add(f"tie_lockstep_{int(round(t * 1000)):04d}", tie_lockstep_trace(make, t), v, full=True)
     return S

@@ -36,7 +36,7 @@ BRANCH_NAMES = (
 )
 TRIGGER_NAMES = ("alg1", "alg2", "monitor:tpot", "monitor:idle", "drained")
 
-OK, STALLED, INCOMPLETE, NOT_DRAINED, NO_INSTANCE, ZERO_DIVISION, BUFFER_OVERFLOW, INTERNAL = range(8)
+OK, STALLED, INCOMPLETE, NOT_DRAINED, NO_INSTANCE, ZERO_DIVISION, BUFFER_OVERFLOW, INTERNAL, AUDIT_FAILED = range(9)
 STATUS_NAMES = (
     "ok",
     "stalled",
@@ -46,6 +46,7 @@ STATUS_NAMES = (
     "zero-division",
     "buffer-overflow",
     "internal",
+    "audit-failed",
 )
 OVERFLOW_NAMES = ("none", "queue", "emission", "fifo", "decisions", "snapshots", "iterlog", "running", "seq")
 

@@ -18,18 +18,20 @@ from ._buffers import HostBuffers, OutputSpec
 from ._compile import CompiledBatch
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libarrow_sim.so"
+# RunConfig.audit=True: the same kernel built with -DARROW_AUDIT (per-step
+# KV / partition checks, engine.py:279-282)
+AUDIT_LIB_PATH = LIB_PATH.with_name("libarrow_sim_audit.so")
 
-_lib = None
+_libs: dict = {}
 
 
 class EvaluatorUnavailable(RuntimeError):
     pass
 
 
-def load_library() -> ctypes.CDLL:
-    global _lib
-    if _lib is None:
-        path = Path(os.environ.get("ARROW_SIM_LIB", LIB_PATH))
+def load_library(audit: bool = False) -> ctypes.CDLL:
+    if audit not in _libs:
+        path = AUDIT_LIB_PATH if audit else Path(os.environ.get("ARROW_SIM_LIB", LIB_PATH))
         if not path.exists():
             raise EvaluatorUnavailable(
                 f"CUDA evaluator library not built: {path} (run `make lib` or __graft_entry__.build())"
@@ -45,9 +47,9 @@ def load_library() -> ctypes.CDLL:
         lib.arrow_sim_status_string.argtypes = [ctypes.c_int]
         lib.arrow_sim_status_string.restype = ctypes.c_char_p
         if lib.arrow_sim_abi_version() != _abi.ABI_VERSION:
-            raise EvaluatorUnavailable("libarrow_sim.so ABI version mismatch; rebuild")
-        _lib = lib
-    return _lib
+            raise EvaluatorUnavailable(f"{path.name} ABI version mismatch; rebuild")
+        _libs[audit] = lib
+    return _libs[audit]
 
 
 _OUTPUT_FIELDS = (
@@ -163,16 +165,18 @@ class CudaEvaluator:
 
     BUILDS = {None: 0, "latency": 1, "throughput": 2}  # ARROW_SIM_FORCE_* (include/arrow_sim.h)
 
-    def __init__(self, device=None, build: str | None = None) -> None:
+    def __init__(self, device=None, build: str | None = None, audit: bool = False) -> None:
         """build: None picks the kernel build by batch size; "latency" /
-        "throughput" force one (identical results, different speed)."""
+        "throughput" force one (identical results, different speed).
+        audit: the per-step checking build (RunConfig.audit)."""
         import torch
 
         self.flags = self.BUILDS[build]
         if not torch.cuda.is_available():
             raise EvaluatorUnavailable("no CUDA device: the Arrow evaluator runs only on the GPU (no CPU fallback)")
         self.torch = torch
-        self.lib = load_library()
+        self.lib = load_library(audit)
+        self.audit = audit
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self._ws = None
 
@@ -222,12 +226,12 @@ class CudaEvaluator:
 _default: dict = {}
 
 
-def default_evaluator() -> CudaEvaluator:
+def default_evaluator(audit: bool = False) -> CudaEvaluator:
     import torch
 
     dev = torch.cuda.current_device() if torch.cuda.is_available() else None
-    ev = _default.get(dev)
+    ev = _default.get((dev, audit))
     if ev is None:
-        ev = CudaEvaluator()
-        _default[dev] = ev
+        ev = CudaEvaluator(audit=audit)
+        _default[(dev, audit)] = ev
     return ev

@@ -57,6 +57,8 @@ def raise_for_status(hb: HostBuffers, s: int) -> None:
         raise RuntimeError("no instance available for prefill dispatch")
     if st == _abi.ZERO_DIVISION:
         raise ZeroDivisionError("division by zero")
+    if st == _abi.AUDIT_FAILED:
+        raise AssertionError("audit: instance KV accounting or pool partition inconsistent (engine.py:279-282)")
     if st == _abi.BUFFER_OVERFLOW:
         raise OverflowError(f"evaluator buffer too small: {_abi.OVERFLOW_NAMES[int(summ['overflow'])]}")
     raise RuntimeError(f"evaluator invariant violated (status {_abi.STATUS_NAMES[st]})")

@@ -292,6 +292,7 @@ const char* arrow_sim_status_string(int status) {
     case ARROW_ZERO_DIVISION: return "zero-division";
     case ARROW_BUFFER_OVERFLOW: return "buffer-overflow";
     case ARROW_INTERNAL: return "internal";
+    case ARROW_AUDIT_FAILED: return "audit-failed";
     default: return "unknown";
   }
 }

@@ -35,6 +35,17 @@
 #include "arrow_sim.h"
 #include "warp.cuh"
 
+// Test-only mutants (host emulator build with -DARROW_MUTANTS, selected by
+// the ARROW_MUTANT environment variable): tests prove that the tie fixture
+// and the audit build can tell them from the shipped source.
+#if !defined(__CUDA_ARCH__) && defined(ARROW_MUTANTS)
+#include <stdlib.h>
+#include <string.h>
+#define MUTANT(name) (getenv("ARROW_MUTANT") != nullptr && strcmp(getenv("ARROW_MUTANT"), name) == 0)
+#else
+#define MUTANT(name) false
+#endif
+
 #if !defined(__CUDA_ARCH__) && defined(ARROW_EMU_TRACE)
 #include <stdio.h>
 #include <stdlib.h>
@@ -179,6 +190,10 @@ struct WarpSmem {
   uint32_t bseq[MAX_INST];       // sequence of its head / final pending push
   uint64_t bfinal[MAX_INST];     // key of its final pushing event (~0: none)
   int btie;
+#ifdef ARROW_AUDIT
+  int aud_parked_kv[MAX_INST];   // audit: KV parked on each instance, recounted from the queues
+  int aud_parked_n[MAX_INST];
+#endif
 };
 
 // Registers of one instance on its owner lane (instance.py:78-92, reshaped).
@@ -593,7 +608,7 @@ struct Sim {
       const int nr = mq_rid(I.id)[I.mq_h];
       I.mq_need = inl[nr] + (outl[nr] - 1);
     }
-    I.kv_reserved += inl[rid];
+    I.kv_reserved += inl[rid] + (MUTANT("kv") ? 1 : 0);   // (mutant "kv": reservation off by one)
     I.mig_active = 1;
     I.mig_rid = rid;
     const arrow_scenario_t& s = sc();
@@ -2211,11 +2226,9 @@ struct Sim {
           for (int a2 = 1; a2 < na; a2++) {
             const int i = act[a2];
             const uint64_t kk = sm->blist[sm->boff[i] + sm->bhead[i]];
-#ifdef ARROW_MUTATE_TIE_REVERSE  // test-only mutant: equal keys merged in reversed order
-            if (kk < bk0 || (kk == bk0 && sm->bseq[i] > sm->bseq[act[best]])) {
-#else
-            if (kk < bk0 || (kk == bk0 && sm->bseq[i] < sm->bseq[act[best]])) {
-#endif
+            // (mutant "tie": equal keys merged in reversed order)
+            if (kk < bk0 || (kk == bk0 && (MUTANT("tie") ? sm->bseq[i] > sm->bseq[act[best]]
+                                                          : sm->bseq[i] < sm->bseq[act[best]]))) {
               best = a2;
               bk0 = kk;
             }
@@ -2276,6 +2289,94 @@ struct Sim {
 
 
 
+#ifdef ARROW_AUDIT
+  // RunConfig.audit (engine.py:279-282): Instance.audit() (instance.py:364-
+  // 378) and PoolSet.check_partition() (pools.py:127-137) after every step.
+  // The incremental counters are recomputed from the queues themselves: KV
+  // held by running decodes (prompt + generated), by the partial and the
+  // pending prefill chunks, by waiting decodes and by prompts parked for a
+  // PREFILL_COMPLETE or a migration (found in the FIFO and in every
+  // instance's migration queue); KV reserved by the active migration; the
+  // growth and running-token sums; pool membership.  A mismatch ends the run
+  // with ARROW_AUDIT_FAILED (the shim raises AssertionError).
+  AS_HD void audit_state() {
+    const int N = sc().n_instances;
+    lane0([&] {
+      for (int i = 0; i < N; i++) sm->aud_parked_kv[i] = sm->aud_parked_n[i] = 0;
+      const Uniform& U = u();
+      for (int c = 0; c < U.fifo_count; c++) {
+        const int slot = ring(U.fifo_head, c, L.n_max);
+        sm->aud_parked_kv[p.fifo_src[slot]] += inl[p.fifo_rid[slot]];
+        sm->aud_parked_n[p.fifo_src[slot]]++;
+      }
+    });
+#pragma unroll
+    for (int k = 0; k < IPL; k++) {
+      const Inst& I = st[k];
+      if (I.id < 0) continue;
+      for (int c = 0; c < I.mq_c + (I.mig_active ? 1 : 0); c++) {
+        const int rid = c < I.mq_c ? mq_rid(I.id)[ring(I.mq_h, c, L.qcap)] : I.mig_rid;
+        w.atomic_add_shared(&sm->aud_parked_kv[p.src[rid]], inl[rid]);
+        w.atomic_add_shared(&sm->aud_parked_n[p.src[rid]], 1);
+      }
+    }
+    w.sync();
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < IPL; k++) {
+      const Inst& I = st[k];
+      if (I.id < 0) continue;
+      const int lc = I.it - 1 - (I.busy ? 1 : 0);      // last completed iteration
+      int64_t held = 0, committed = 0, rtok = 0, wgrowth = 0;
+      for (int j = 0; j < I.R; j++) {                  // running decodes
+        const int rid = run_rid(I.id)[j];
+        const int f = run_f(I.id)[j];
+        const int g = outl[rid] - 1;
+        const int gen = g - (f - lc);
+        bad = bad || gen < 0 || gen >= g;
+        held += inl[rid] + gen;
+        committed += f - lc;
+        rtok += inl[rid] + gen;
+      }
+      for (int j = 0; j < I.wd_c; j++) {               // waiting decodes hold their prompt
+        const int rid = wd_rid(I.id)[ring(I.wd_h, j, L.qcap)];
+        held += inl[rid];
+        wgrowth += outl[rid] - 1;
+        rtok += inl[rid];
+      }
+      if (I.rp_rid >= 0) held += I.rp_done + (I.busy ? I.pb_rp_chunk : 0);
+      if (I.busy)                                      // prompts admitted by the pending batch
+        for (int j = 0; j < I.pb_k; j++) held += j < I.pb_k - 1 ? inl[wp_rid(I.id)[ring(I.wp_h, j, L.qcap)]] : I.pb_last_chunk;
+      held += sm->aud_parked_kv[I.id];
+      bad = bad || held != I.kv_used || committed != I.committed || rtok != I.rtok || wgrowth != I.wgrowth;
+      bad = bad || sm->aud_parked_n[I.id] != I.parked;
+      bad = bad || I.kv_reserved != (I.mig_active ? inl[I.mig_rid] : 0);
+      bad = bad || I.kv_used < 0 || I.kv_reserved < 0 || I.kv_used + I.kv_reserved > sc().kv_capacity;
+      bad = bad || I.pool != sm->pool_of[I.id] || I.pool < 0 || I.pool > 3;
+    }
+    if (lane == 0) {                                   // partition: counts and distinct positions per pool
+      int cnt[4] = {0, 0, 0, 0};
+      for (int i = 0; i < N; i++) {
+        const int pk = sm->pool_of[i];
+        if (pk < 0 || pk > 3) {
+          bad = true;
+          continue;
+        }
+        cnt[pk]++;
+        for (int j = 0; j < i; j++) bad = bad || (sm->pool_of[j] == pk && sm->pos_of[j] == sm->pos_of[i]);
+      }
+      for (int q = 0; q < 4; q++) bad = bad || cnt[q] != u().pool_n[q];
+    }
+    if (w.any(bad)) lane0([&] { set_status(ARROW_AUDIT_FAILED); });
+    w.sync();
+  }
+#define AUDIT_STEP() audit_state()
+#else
+#define AUDIT_STEP() \
+  do {               \
+  } while (0)
+#endif
+
   AS_HD void simulate() {
     const int64_t limit = sc().stall_limit;
     Head h = full_scan();
@@ -2291,6 +2392,7 @@ struct Sim {
         if (bsel) {
           PROF_CLOCK(cb);
           run_burst(part, hz, per, h);
+          AUDIT_STEP();
           PROF_MARK(9, cb);
           PROF_ADD(cyc_burst, c0);
           const int status = u().status;
@@ -2303,6 +2405,7 @@ struct Sim {
         PROF_MARK(10, cr);
         PROF_CLOCK(cx);
         run_round(part, h);
+        AUDIT_STEP();
         PROF_MARK(11, cx);
         PROF_ADD(cyc_round, c0);
         const int status = u().status;
@@ -2391,6 +2494,7 @@ struct Sim {
         }
       }
       serial_tail(tm0, tm1, tk0, tk1, now);
+      AUDIT_STEP();
       const int status = u().status;
       const int64_t esp = u().esp;
       w.sync();

@@ -55,8 +55,10 @@ def execute(scenarios: list[Scenario], spec: OutputSpec, evaluator=None, order=N
     run reports an overflow.  Returns (CompiledBatch, HostBuffers)."""
     from ._backend import default_evaluator
 
-    ev = evaluator or default_evaluator()
     cb = compile_batch(scenarios, STALL_EVENT_LIMIT)
+    # RunConfig.audit (engine.py:279-282): the per-step checking build
+    audit = any(getattr(sc.config, "audit", False) for sc in scenarios)
+    ev = evaluator or (default_evaluator(audit=True) if audit else default_evaluator())
     if order is None and cb.n > 1:
         order = dispatch_order(cb)
     while True:

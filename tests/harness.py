@@ -32,7 +32,7 @@ _libs: dict = {}
 
 
 def _build(target: str) -> None:
-    subprocess.run(["make", "-s", "-C", str(ROOT), target], check=True)
+    subprocess.run(["make", "-s", "-j8", "-C", str(ROOT), target], check=True)
 
 
 def oracle_lib() -> ctypes.CDLL:
@@ -55,12 +55,14 @@ def oracle_lib() -> ctypes.CDLL:
 def emu_lib(variant: str = "") -> ctypes.CDLL:
     """variant "" is the kernel source as shipped; "wide" widens the delay
     intervals so that most dispatch decisions take the exact-fold fallback;
-    "mut" merges equal-time burst finals in reversed order (a mutant the tie
-    fixture must catch)."""
+    "mut" carries test-only mutants selected per call (run_emu(mutant=...)):
+    "tie" merges equal-time burst finals in reversed order, "kv" mis-reserves
+    migration KV (the audit checks are compiled in); "audit" is the shipped
+    source with the per-step audit checks."""
     key = "emu" + variant
     if key not in _libs:
         path = ROOT / "build" / {"": "libarrow_emu.so", "wide": "libarrow_emu_wide.so",
-                                 "mut": "libarrow_emu_mut.so"}[variant]
+                                 "mut": "libarrow_emu_mut.so", "audit": "libarrow_emu_audit.so"}[variant]
         _build("emu")
         lib = ctypes.CDLL(str(path))
         lib.arrow_emu_run.argtypes = [ctypes.c_void_p, ctypes.c_int]
@@ -125,10 +127,19 @@ def run_oracle_timed(cb, threads=0):
     return hb, secs, used
 
 
-def run_emu(cb, spec=FULL, width=8, variant: str = "") -> HostBuffers:
+def run_emu(cb, spec=FULL, width=8, variant: str = "", mutant: str | None = None) -> HostBuffers:
+    """mutant (variant "mut" only): ARROW_MUTANT=tie|kv for this call."""
+    import os
+
     hb = HostBuffers(cb, spec)
     b = hb.host_struct()
-    rc = emu_lib(variant).arrow_emu_run(ctypes.addressof(b), width)
+    if mutant:
+        assert variant == "mut"
+        os.environ["ARROW_MUTANT"] = mutant
+    try:
+        rc = emu_lib(variant).arrow_emu_run(ctypes.addressof(b), width)
+    finally:
+        os.environ.pop("ARROW_MUTANT", None)
     assert rc == 0, rc
     return hb
 
@@ -263,4 +274,4 @@ def use_oracle_backend(monkeypatch) -> None:
     from paper_2505_11916_b200 import _backend
 
     ev = OracleEvaluator()
-    monkeypatch.setattr(_backend, "default_evaluator", lambda: ev)
+    monkeypatch.setattr(_backend, "default_evaluator", lambda audit=False: ev)

@@ -60,7 +60,7 @@ def test_struct_layout_matches_python_mirrors(lib):
 def test_status_strings(lib):
     lib.arrow_sim_status_string.restype = ctypes.c_char_p
     lib.arrow_sim_status_string.argtypes = [ctypes.c_int]
-    assert [lib.arrow_sim_status_string(i).decode() for i in range(8)] == list(_abi.STATUS_NAMES)
+    assert [lib.arrow_sim_status_string(i).decode() for i in range(len(_abi.STATUS_NAMES))] == list(_abi.STATUS_NAMES)
 
 
 def test_library_is_sm100a():
