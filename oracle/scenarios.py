@@ -373,6 +373,18 @@ def catalogue_r2(make, c5_count=32, which=("c3", "c4", "c5", "tie")):
         for sid in c5_stratified_ids(c5_count):
             tr, v, sc = c5_scenario(make, sid, traces)
             add(f"c5_{sid:05d}", tr, v, scale=sc)
+    if "adv" in which:
+        # Adversarial predictors for the delay-interval bound (sim_core.cuh:
+        # delay_interval): heavy profiling noise makes the fitted a2 / a1 / a0
+        # negative (e.g. a0 = -0.15 s, a2 < 0), so predicted prefill terms of
+        # the delay fold have mixed signs and cancel.
+        tr = bursty(make)[:300]
+        for k, (noise, seed) in enumerate([(1.0, 1), (1.0, 2), (1.0, 3), (3.0, 0), (3.0, 1), (3.0, 2), (3.0, 3),
+                                           (10.0, 5)]):
+            strat = "minimal-load" if k % 4 == 3 else "slo-aware"
+            v = cfg(instances=4 + k % 4, init_prefill=2 + k % 2, init_decode=2 + k % 4 - k % 2, strategy=strat,
+                    profile_noise=noise, seed=seed, kv_capacity_tokens=3000, a2=2e-8, a1=2e-5, a0=2e-3)
+            add(f"adv_delay_{k}", tr, v, scale=rate_scale(tr, 6.0 + 2 * k), full=k % 2 == 0)
     if "tie" in which:
         v = cfg(instances=2, init_prefill=2, init_decode=0, enable_flips=False, **ENGINE_TEST)
         for t in TIE_ARRIVALS:

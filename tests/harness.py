@@ -32,7 +32,14 @@ _libs: dict = {}
 
 
 def _build(target: str) -> None:
-    subprocess.run(["make", "-s", "-j8", "-C", str(ROOT), target], check=True)
+    """Incremental build under a file lock: pytest-xdist workers must not
+    rebuild (and dlopen) the same library concurrently."""
+    import fcntl
+
+    (ROOT / "build").mkdir(exist_ok=True)
+    with open(ROOT / "build" / ".build.lock", "w") as lock:
+        fcntl.flock(lock, fcntl.LOCK_EX)
+        subprocess.run(["make", "-s", "-j8", "-C", str(ROOT), target], check=True)
 
 
 def oracle_lib() -> ctypes.CDLL:

@@ -87,7 +87,7 @@ def test_emulated_kernel_matches_oracle_on_c2_points(index):
         H.assert_same_decisions(got.decisions_of(0), exp.decisions_of(0))
 
 
-WIDE = [m for m in SMALL if m["name"].startswith(("fuzz_", "overload", "c1_", "small_", "migration", "tight"))]
+WIDE = [m for m in SMALL if m["name"].startswith(("fuzz_", "overload", "c1_", "small_", "migration", "tight", "adv_delay"))]
 
 
 @pytest.mark.parametrize("meta", WIDE, ids=[m["name"] for m in WIDE])
@@ -128,3 +128,17 @@ def test_emulated_kernel_lockstep_instances_match_oracle():
     exp = H.run_oracle(cb, spec)
     H.assert_same_run(got, exp, cb.n)
     assert (exp.summaries["status"] == 0).all()
+
+
+def test_emulated_kernel_adversarial_predictors_match_oracle():
+    """Mixed-sign, cancelling predictor terms (heavy profiling noise) through
+    the kernel source, shipped and wide-interval builds, against the oracle."""
+    from test_gpu_sweeps import _adversarial_predictor_scenarios, _compare
+    from paper_2505_11916_b200._buffers import OutputSpec
+    from paper_2505_11916_b200._compile import compile_batch
+
+    cb = compile_batch(_adversarial_predictor_scenarios(12, 12), 20000)
+    spec = OutputSpec(requests=True)
+    exp = H.run_oracle(cb, spec, threads=0)
+    for variant in ("", "wide"):
+        _compare(H.run_emu(cb, spec, width=8, variant=variant), exp, cb.n)

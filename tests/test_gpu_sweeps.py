@@ -79,3 +79,36 @@ def test_c3_sample_matches_oracle(evaluator):
     (Arrow re-simulated per SLO point: thresholds and token cap follow)."""
     ids = np.sort(np.random.default_rng(3).choice(1920, size=192, replace=False))
     _run(evaluator, W.c3(ids))
+
+
+def _adversarial_predictor_scenarios(seed: int, count: int):
+    """Heavy profiling noise (profile_noise 1-10) fits predictors with
+    negative a2 / a1 / a0: predicted prefill terms of mixed sign that cancel
+    in the delay fold, the case the delay-interval bound must survive."""
+    import sys
+
+    sys.path.insert(0, str(H.ROOT / "oracle"))
+    import scenarios as S
+    from paper_2505_11916_b200._compile import Scenario
+    from paper_2505_11916_b200.config import config_from_values
+    from paper_2505_11916_b200.core import TraceRequest
+
+    rng = np.random.default_rng(seed)
+    tr = S.bursty(TraceRequest)[:400]
+    out = []
+    for k in range(count):
+        N = int(rng.integers(2, 13))
+        n_p = int(rng.integers(1, N))
+        v = S.cfg(instances=N, init_prefill=n_p, init_decode=N - n_p,
+                  strategy=["slo-aware", "slo-aware", "minimal-load"][k % 3],
+                  profile_noise=float(rng.choice([1.0, 3.0, 10.0])), seed=int(rng.integers(0, 50)),
+                  kv_capacity_tokens=int(rng.choice([3000, 8000])), a2=2e-8, a1=2e-5, a0=2e-3,
+                  ttft_slo=float(rng.choice([0.5, 3.0])))
+        out.append(Scenario(tr, config_from_values(v), S.rate_scale(tr, float(rng.uniform(0.5, 3.0)) * N), k))
+    return out
+
+
+def test_adversarial_predictor_sweep_matches_oracle(evaluator):
+    cb = compile_batch(_adversarial_predictor_scenarios(11, 256), 20000)
+    spec = OutputSpec(requests=True)
+    _compare(evaluator.execute(cb, spec), H.run_oracle(cb, spec, threads=0), cb.n)
