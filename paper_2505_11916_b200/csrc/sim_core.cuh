@@ -1512,15 +1512,20 @@ struct Sim {
       I.mig_rid = -1;
       I.pool = I.id >= 0 ? pool_of(I.id) : -1;
     }
-    int32_t* rpf = (have_om && om.req_offset >= 0) ? B->req_prefill : 0;
-    int32_t* rdc = (have_om && om.req_offset >= 0) ? B->req_decode : 0;
-    int32_t* rdi = (have_om && om.req_offset >= 0) ? B->req_decode_iter : 0;
-    for (int r = lane; r < c.n_requests; r += WD) {
-      p.first[r] = NAN;
-      p.last[r] = NAN;
-      if (rpf) rpf[om.req_offset + r] = -1;
-      if (rdc) rdc[om.req_offset + r] = -1;
-      if (rdi) rdi[om.req_offset + r] = -1;
+    // Per-request state starts as "no token yet" only where it can be
+    // observed: per-request outputs of a run that stops early.  A completed
+    // run writes every first / last time before summarize() reads them.
+    if (have_om && om.req_offset >= 0) {
+      int32_t* rpf = B->req_prefill;
+      int32_t* rdc = B->req_decode;
+      int32_t* rdi = B->req_decode_iter;
+      for (int r = lane; r < c.n_requests; r += WD) {
+        p.first[r] = NAN;
+        p.last[r] = NAN;
+        if (rpf) rpf[om.req_offset + r] = -1;
+        if (rdc) rdc[om.req_offset + r] = -1;
+        if (rdi) rdi[om.req_offset + r] = -1;
+      }
     }
     w.sync();
   }
