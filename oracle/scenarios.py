@@ -385,6 +385,22 @@ def catalogue_r2(make, c5_count=32, which=("c3", "c4", "c5", "tie")):
             v = cfg(instances=4 + k % 4, init_prefill=2 + k % 2, init_decode=2 + k % 4 - k % 2, strategy=strat,
                     profile_noise=noise, seed=seed, kv_capacity_tokens=3000, a2=2e-8, a1=2e-5, a0=2e-3)
             add(f"adv_delay_{k}", tr, v, scale=rate_scale(tr, 6.0 + 2 * k), full=k % 2 == 0)
+    if "stallchunk" in which:
+        # Long prompts in small chunks: runs of token-less prefill iterations
+        # that only advance the stall counter (engine.py:268).  With small
+        # watchdog limits the reference raises mid-prefill, so the exact
+        # event at which the counter crosses the limit is pinned.
+        for k, limit in enumerate((130, 150, 200, 257, 300, 400, 1000)):
+            n = 2 + k % 3
+            reqs = [make(i, 0.05 * i, 6000 - 500 * (i % 4), 3 + i % 5) for i in range(6 + k)]
+            v = cfg(instances=n, init_prefill=n - 1, init_decode=1, chunk_budget=32 + 16 * (k % 3),
+                    kv_capacity_tokens=16000, **ENGINE_TEST)
+            add(f"stallchunk_{k}", reqs, v, stall_limit=limit, full=True)
+        for k, (limit, n_p) in enumerate(((300, 2), (400, 2), (500, 3), (700, 3), (333, 1))):
+            reqs = [make(i, 0.01 * i, 8000 - 7 * i, 2 + i % 3) for i in range(8)]
+            v = cfg(instances=n_p + 1, init_prefill=n_p, init_decode=1, chunk_budget=32, kv_capacity_tokens=40000,
+                    **ENGINE_TEST)
+            add(f"stallchunk_long_{k}", reqs, v, stall_limit=limit, full=True)
     if "tie" in which:
         v = cfg(instances=2, init_prefill=2, init_decode=0, enable_flips=False, **ENGINE_TEST)
         for t in TIE_ARRIVALS:
