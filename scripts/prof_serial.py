@@ -1,6 +1,9 @@
 """Serial-step cycle breakdown by event kind (needs a -DARROW_PROF build).
 
-    ARROW_SIM_LIB=/tmp/libprof.so python scripts/prof_serial.py
+    ARROW_SIM_LIB=/tmp/libprof.so python scripts/prof_serial.py [c2|c5 [sample]]
+
+c5: a seeded sample (default 4 096) of the C5 sweep through the occupancy
+build; also prints the step counts (serial / parallel) and per-kind shares.
 """
 import ctypes
 import os
@@ -21,7 +24,13 @@ def main():
     from paper_2505_11916_b200._buffers import OutputSpec
     from paper_2505_11916_b200._compile import compile_batch, dispatch_order
 
-    scen = W.c2(trace=W.c2_variant_trace(0))
+    which = sys.argv[1] if len(sys.argv) > 1 else "c2"
+    if which == "c5":
+        n = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
+        ids = np.sort(np.random.default_rng(5).choice(98304, size=n, replace=False))
+        scen = W.c5(ids)
+    else:
+        scen = W.c2(trace=W.c2_variant_trace(0))
     ev = CudaEvaluator()
     cb = compile_batch(scen, engine.STALL_EVENT_LIMIT)
     hb = ev.execute(cb, OutputSpec(), dispatch_order(cb))
@@ -39,6 +48,9 @@ def main():
         print(f"scenario {k}: {tot / 1e6:.1f}M cycles: {parts}")
     agg = p.sum(0) / cyc.sum()
     print("all:", ", ".join(f"{names[q]} {100 * agg[q]:.1f}%" for q in range(16) if names[q] != "-"))
+    s = hb.summaries
+    print("events %d serial steps %d parallel steps %d bursts+rounds; cycles/event %.0f" % (
+        s["n_events"].sum(), s["n_serial_steps"].sum(), s["n_parallel_steps"].sum(), cyc.sum() / s["n_events"].sum()))
 
 
 if __name__ == "__main__":
