@@ -395,4 +395,5 @@ def dispatch_order(cb: CompiledBatch) -> np.ndarray:
         est[k] = total_out / (1.0 + per_inst)
     policy = cb.scenarios["strategy"].astype(np.int64) * 2 + cb.scenarios["enable_flips"].astype(np.int64)
     trace = np.asarray(cb.trace_index, dtype=np.int64)
-    return np.lexsort((-est, trace, policy)).astype(np.int32)
+    wide = (cb.scenarios["n_instances"] > 32).astype(np.int64)     # two instances per lane
+    return np.lexsort((-est, trace, policy, -wide)).astype(np.int32)
