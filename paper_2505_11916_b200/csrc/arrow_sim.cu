@@ -305,6 +305,6 @@ const char* arrow_sim_status_string(int status) {
 // migration, rescan), copied out after a launch.
 extern "C" int arrow_sim_prof(int64_t* out, int n) {
   if (n > ARROW_PROF_MAX) n = ARROW_PROF_MAX;
-  return (int)cudaMemcpyFromSymbol(out, arrow_prof_cycles, (size_t)n * 16 * sizeof(int64_t));
+  return (int)cudaMemcpyFromSymbol(out, arrow_prof_cycles, (size_t)n * 32 * sizeof(int64_t));
 }
 #endif

@@ -61,7 +61,7 @@
 
 #if defined(ARROW_PROF) && defined(__CUDACC__)
 #define ARROW_PROF_MAX 4096
-__device__ int64_t arrow_prof_cycles[ARROW_PROF_MAX * 16];
+__device__ int64_t arrow_prof_cycles[ARROW_PROF_MAX * 32];
 #endif
 
 namespace arrow {
@@ -160,7 +160,7 @@ struct Uniform {
   int64_t rr_p, rr_d;
   int64_t n_rounds, n_serial, n_bursts;
   int64_t cyc_serial, cyc_round, cyc_burst;   // profiling: SM cycles by step kind
-  int64_t cyc_kind[16];                       // ARROW_PROF: serial cycles by event kind, rescan, selection/execution
+  int64_t cyc_kind[32];                       // ARROW_PROF: serial cycles by event kind, rescan, selection/execution
   uint64_t hash;
   uint32_t seq, tick_seq;
   int a;
@@ -1261,7 +1261,9 @@ struct Sim {
       U.a = rid + 1;
       U.next_arrival = U.a < sc().n_requests ? arr[U.a] * sc().arrival_scale : 0.0;
     });
+    PROF_CLOCK(ps0);
     int target = schedule_prefill(rid, now, own);
+    PROF_MARK(16, ps0);
     if (target < 0) return -1;
     owner(target, [&](Inst& I) {
       if (I.wp_c >= L.qcap) {
@@ -1292,7 +1294,9 @@ struct Sim {
       U.fifo_head = U.fifo_head + 1 == L.n_max ? 0 : U.fifo_head + 1;
       U.fifo_count--;
     });
+    PROF_CLOCK(ps1);
     int target = schedule_decode(rid, src, now);
+    PROF_MARK(17, ps1);
     const int in = inl[rid], g = outl[rid] - 1;
     owner(target, [&](Inst& I) {
       if (target == src) {
@@ -2431,6 +2435,8 @@ struct Sim {
       });
 #ifdef ARROW_PROF
       const int prof_kind = ev >= 1000 ? ev - 1000 : ((ev & 1) ? 5 : 6);
+      if (lane == 0) u().cyc_kind[24 + prof_kind] += 1;   // event counts by kind
+      PROF_MARK(20, c0);                                   // selection + bookkeeping up to here
 #endif
       int tm0 = -1, tm1 = -1, tk0 = -1, tk1 = -1;   // serial_tail() arguments
       if (ev >= 1000) {
@@ -2479,6 +2485,7 @@ struct Sim {
         int id = ev >> 1;
         if (ev & 1) {
           int dst = -1;
+          PROF_CLOCK(pi0);
           owner(id, [&](Inst& I) {
             int completed = 0;
             bool pushed = false;
@@ -2490,6 +2497,7 @@ struct Sim {
           });
           dst = u().tmp_i[0];
           w.sync();
+          PROF_MARK(19, pi0);
           if (dst >= 0) move_and_log(id, dst, now, ARROW_TRIG_DRAINED);
           tm0 = tk0 = id;
         } else {
@@ -2498,7 +2506,9 @@ struct Sim {
           tm1 = tk1 = src;
         }
       }
+      PROF_CLOCK(pt0);
       serial_tail(tm0, tm1, tk0, tk1, now);
+      PROF_MARK(18, pt0);
       AUDIT_STEP();
       const int status = u().status;
       const int64_t esp = u().esp;
@@ -2671,7 +2681,7 @@ struct Sim {
       out->cycles = clock_now() - t_start;
 #if defined(ARROW_PROF) && defined(__CUDA_ARCH__)
       if (sid < ARROW_PROF_MAX)
-        for (int q = 0; q < 16; q++) arrow_prof_cycles[sid * 16 + q] = U.cyc_kind[q];
+        for (int q = 0; q < 32; q++) arrow_prof_cycles[sid * 32 + q] = U.cyc_kind[q];
 #endif
       {  // profiling: per-mille of loop cycles in serial steps (high word) and rounds (low word)
         const int64_t tot = U.cyc_serial + U.cyc_round + U.cyc_burst + 1;

@@ -27,7 +27,7 @@ def main():
     scen, _ = bench.workload("c5")
     ev = CudaEvaluator()
     cb = compile_batch(scen, engine.STALL_EVENT_LIMIT)
-    base = dispatch_order(cb)
+    base = dispatch_order(cb)          # shipped: (wide, policy, trace) groups, longest-first
     rank = np.empty(cb.n, dtype=np.int64)
     rank[base] = np.arange(cb.n)                       # longest-first position
     strat = cb.scenarios["strategy"].astype(np.int64)
@@ -35,14 +35,14 @@ def main():
     pol = strat * 2 + flips
     N = cb.scenarios["n_instances"].astype(np.int64)
     tr = np.asarray(cb.trace_index, dtype=np.int64)
+    scale = cb.scenarios["arrival_scale"]
+    theta = cb.scenarios["theta_d"] * 16 + cb.scenarios["theta_busy"] * 4 + cb.scenarios["breach_duration"]
     orders = {
-        "longest_first": base,
-        "policy_then_longest": np.lexsort((rank, pol)).astype(np.int32),
-        "N_then_longest": np.lexsort((rank, -N)).astype(np.int32),
-        "policyN_then_longest": np.lexsort((rank, -N, pol)).astype(np.int32),
+        "shipped": base,
+        "policy_trace_scale": np.lexsort((scale, tr, pol)).astype(np.int32),
+        "policy_trace_N_scale": np.lexsort((scale, -N, tr, pol)).astype(np.int32),
+        "policy_trace_longest_theta": np.lexsort((theta, rank, tr, pol)).astype(np.int32),
         "policy_trace_then_longest": np.lexsort((rank, tr, pol)).astype(np.int32),
-        "policy_N_trace_then_longest": np.lexsort((rank, tr, -N, pol)).astype(np.int32),
-        "trace_then_longest": np.lexsort((rank, tr)).astype(np.int32),
     }
     res = {}
     for rep in range(2):

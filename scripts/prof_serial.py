@@ -35,19 +35,27 @@ def main():
     cb = compile_batch(scen, engine.STALL_EVENT_LIMIT)
     hb = ev.execute(cb, OutputSpec(), dispatch_order(cb))
     lib = load_library()
-    out = np.zeros(len(scen) * 16, dtype=np.int64)
+    out = np.zeros(len(scen) * 32, dtype=np.int64)
     rc = lib.arrow_sim_prof(out.ctypes.data_as(ctypes.c_void_p), len(scen))
     assert rc == 0, rc
-    p = out.reshape(-1, 16)
-    names = ["rr_iter", "rr_rank", "prefill_c", "arrival", "tick", "loud_iter", "migration", "rescan", "burst_sel", "burst_run", "round_sel", "round_run", "chains", "merge", "delays", "load_low"]
+    p = out.reshape(-1, 32)
+    names = ["rr_iter", "rr_rank", "prefill_c", "arrival", "tick", "loud_iter", "migration", "rescan", "burst_sel",
+             "burst_run", "round_sel", "round_run", "chains", "merge", "delays", "load_low", "sched_prefill",
+             "sched_decode", "serial_tail", "iter_serial", "select_book"] + ["-"] * 11
     cyc = hb.summaries["cycles"]
     top = np.argsort(-cyc)[:6]
     for k in top:
         tot = cyc[k]
-        parts = ", ".join(f"{names[q]} {100 * p[k, q] / tot:.1f}%" for q in range(16) if names[q] != "-")
+        parts = ", ".join(f"{names[q]} {100 * p[k, q] / tot:.1f}%" for q in range(21) if names[q] != "-")
         print(f"scenario {k}: {tot / 1e6:.1f}M cycles: {parts}")
     agg = p.sum(0) / cyc.sum()
-    print("all:", ", ".join(f"{names[q]} {100 * agg[q]:.1f}%" for q in range(16) if names[q] != "-"))
+    print("all:", ", ".join(f"{names[q]} {100 * agg[q]:.1f}%" for q in range(21) if names[q] != "-"))
+    cnt = p[:, 24:32].sum(0)
+    kinds = ["iter?", "-", "prefill_c", "arrival", "tick", "loud_iter", "migration", "-"]
+    tot_cyc = cyc.sum()
+    for q in (2, 3, 4, 5, 6):
+        if cnt[q]:
+            print(f"  {kinds[q]:10s} events {cnt[q]:12d}  cycles/event {p[:, q].sum() / cnt[q]:8.0f}")
     s = hb.summaries
     print("events %d serial steps %d parallel steps %d bursts+rounds; cycles/event %.0f" % (
         s["n_events"].sum(), s["n_serial_steps"].sum(), s["n_parallel_steps"].sum(), cyc.sum() / s["n_events"].sum()))
