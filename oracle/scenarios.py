@@ -406,3 +406,49 @@ def catalogue_r2(make, c5_count=32, which=("c3", "c4", "c5", "tie")):
         for t in TIE_ARRIVALS:
             add(f"tie_lockstep_{int(round(t * 1000)):04d}", tie_lockstep_trace(make, t), v, full=True)
     return S
+
+
+# Whole-sweep restatements by scenario id (paper_2505_11916_b200/workloads.py
+# c3 / c4, restated with flat reference config values) for the digest
+# fixtures of oracle/gen_golden_digest.py.
+C3_RATES = (2.0, 4.0, 6.0, 8.0, 10.0, 12.0, 14.0, 16.0)
+C3_TTFT = (0.25, 0.5, 1.0, 2.0, 3.0, 5.0, 10.0, 30.0)
+C3_TPOT = (0.025, 0.05, 0.075, 0.1, 0.15)
+C4_N = (16, 24, 32, 48, 64)
+C4_THETA_D = (0.25, 0.5, 0.75, 1.0)
+C4_THETA_BUSY = (0.5, 0.75, 0.9)
+C4_BREACH = (1.0, 2.0, 4.0)
+C4_TTFT_FACTOR = (0.5, 0.75, 1.0)
+C4_RATE_FACTOR = (1.25, 2.5)
+
+
+def c3_scenario(make, sid, traces=None):
+    """C3 id -> mixed radix (trace 2, rate 8, ttft 8, tpot 5, policy 3)."""
+    x = int(sid)
+    tr, x = x % 2, x // 2
+    k, x = x % 8, x // 8
+    a, x = x % 8, x // 8
+    b, x = x % 5, x // 5
+    pol = x % 3
+    if traces is None:
+        traces = [code_like(make), conversation_like(make)]
+    trace = traces[tr]
+    v = policy_values(C5_POLICIES[pol], 8, ttft_slo=C3_TTFT[a], tpot_slo=C3_TPOT[b])
+    return trace, v, rate_scale(trace, C3_RATES[k])
+
+
+def c4_scenario(make, sid, trace=None):
+    """C4 id -> mixed radix (N 5, theta_d 4, theta_busy 3, breach 3, ttft factor 3, rate 2), Arrow."""
+    x = int(sid)
+    ni, x = x % 5, x // 5
+    td, x = x % 4, x // 4
+    tb, x = x % 3, x // 3
+    br, x = x % 3, x // 3
+    tf, x = x % 3, x // 3
+    rf = x % 2
+    n = C4_N[ni]
+    if trace is None:
+        trace = c4_trace(make)
+    v = policy_values("arrow", n, theta_d=C4_THETA_D[td], theta_busy=C4_THETA_BUSY[tb],
+                      tpot_breach_duration_s=C4_BREACH[br], ttft_threshold=C4_TTFT_FACTOR[tf] * DEFAULTS["ttft_slo"])
+    return trace, v, rate_scale(trace, C4_RATE_FACTOR[rf] * n)

@@ -112,3 +112,40 @@ def test_adversarial_predictor_sweep_matches_oracle(evaluator):
     cb = compile_batch(_adversarial_predictor_scenarios(11, 256), 20000)
     spec = OutputSpec(requests=True)
     _compare(evaluator.execute(cb, spec), H.run_oracle(cb, spec, threads=0), cb.n)
+
+
+# Whole sweeps against the REAL reference: tests/golden/digest_<set>.npz
+# (oracle/gen_golden_digest.py) holds, for every scenario of C3 (1 920) and
+# C4 (1 080) and 512 seeded C5 ids, the reference's status / stall time,
+# every RunSummary field and the FNV-1a digest of its decision stream.
+DIGEST_FIELDS = (("attainment", "attainment"), ("p90_ttft", "p90_ttft"), ("p90_tpot", "p90_tpot"),
+                 ("mean_ttft", "mean_ttft"), ("mean_tpot", "mean_tpot"), ("goodput", "goodput"), ("span", "span_s"))
+
+
+def _digest(name):
+    path = H.GOLDEN / f"digest_{name}.npz"
+    if not path.exists():
+        pytest.skip(f"{path.name} not generated")
+    with np.load(path) as z:
+        return {k: z[k] for k in z.files}
+
+
+def check_against_digest(summaries, d):
+    st = summaries["status"].astype(np.int64)
+    np.testing.assert_array_equal(st, d["status"], err_msg="status (ok / stalled)")
+    ok = d["status"] == 0
+    H.assert_same_f64(summaries["stall_time"][~ok], d["stall_time"][~ok], "stall time")
+    np.testing.assert_array_equal(summaries["decision_hash"][ok], d["decision_hash"][ok], err_msg="decision digest")
+    np.testing.assert_array_equal(summaries["n_decisions"][ok], d["n_decisions"][ok], err_msg="n_decisions")
+    np.testing.assert_array_equal(summaries["n_flips"][ok], d["n_flips"][ok], err_msg="n_flips")
+    for f, g in DIGEST_FIELDS:
+        H.assert_same_f64(summaries[f][ok], d[g][ok], f)
+
+
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+def test_whole_sweep_matches_reference_digest(evaluator, name):
+    d = _digest(name)
+    scs = getattr(W, name)(d["id"])
+    cb = compile_batch(scs, engine.STALL_EVENT_LIMIT)
+    got = evaluator.execute(cb, OutputSpec(), dispatch_order(cb))
+    check_against_digest(got.summaries, d)

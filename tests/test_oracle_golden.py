@@ -113,3 +113,21 @@ def test_decision_hash_definition():
     assert fnv_decision_hash(dec) == int(hb.summaries[0]["decision_hash"])
     lib = H.oracle_lib()
     assert lib.pdsim_oracle_decision_hash(dec.ctypes.data, len(dec)) == int(hb.summaries[0]["decision_hash"])
+
+
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+def test_oracle_matches_reference_digest_sample(name):
+    """Every 16th scenario of the whole-sweep reference digests through the
+    CPU oracle (the B200 runs all of them: test_gpu_sweeps.py)."""
+    from paper_2505_11916_b200 import engine
+    from paper_2505_11916_b200 import workloads as W
+    from paper_2505_11916_b200._buffers import OutputSpec
+    from paper_2505_11916_b200._compile import compile_batch
+
+    import test_gpu_sweeps as T
+
+    d = T._digest(name)
+    sel = np.arange(0, len(d["id"]), 16)
+    d = {k: v[sel] for k, v in d.items()}
+    cb = compile_batch(getattr(W, name)(d["id"]), engine.STALL_EVENT_LIMIT)
+    T.check_against_digest(H.run_oracle(cb, OutputSpec(), threads=0).summaries, d)
