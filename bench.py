@@ -8,7 +8,8 @@ Workload (default): BASELINE.json configs[4] = C5, the 10^5-scenario sweep
 PD-colocated} x N in {4,8,16,32} x theta_d x theta_busy x breach; 255 M
 simulated requests; reference 500 000-event stall watchdog), the
 north-star configuration.  Under torchrun the sweep is sharded statically
-(scenario i -> rank i mod N, total work fixed: "scaling": "strong") and the
+and cost-aware (scenarios sorted by estimated device time and dealt round-
+robin, sweep.balanced_shards; total work fixed: "scaling": "strong") and the
 per-scenario summaries are all-gathered over NCCL (all_gather_into_tensor of
 padded shards) inside every timed step -- the sweep's only collective.
 C1-C4 are the other BASELINE configs (--workload).
@@ -357,7 +358,8 @@ def run_ours(args, rank: int, world: int) -> None:
     from paper_2505_11916_b200._buffers import OutputSpec
     from paper_2505_11916_b200._compile import compile_batch, dispatch_order
     from paper_2505_11916_b200.sweep import (assemble_gathered, evaluate_scenarios, gather_summaries,
-                                             gather_summaries_into, shard, shard_bytes)
+                                             balanced_shards, gather_summaries_into, shard_bytes)
+    from paper_2505_11916_b200._compile import dispatch_estimate
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -366,10 +368,19 @@ def run_ours(args, rank: int, world: int) -> None:
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("ARROW_BENCH_BACKEND", "nccl")   # gloo: N>1 code path on one GPU (tests)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     all_scenarios, desc = workload(args.workload)
     n_total = len(all_scenarios)
-    mine = shard(n_total, rank, world)
+    shards = None
+    if world > 1:   # every rank computes the same split from the whole sweep
+        shards = balanced_shards(dispatch_estimate(compile_batch(all_scenarios, engine.STALL_EVENT_LIMIT))[0], world)
+        mine = shards[rank]
+    else:
+        mine = np.arange(n_total)
     scenarios = [all_scenarios[i] for i in mine]
     ev = CudaEvaluator(dev)
     cb = compile_batch(scenarios, engine.STALL_EVENT_LIMIT)
@@ -419,7 +430,7 @@ def run_ours(args, rank: int, world: int) -> None:
     value = total_req / (ms_max / 1000.0)
 
     if world > 1:
-        full = assemble_gathered(gathered.cpu().numpy(), n_total, world)
+        full = assemble_gathered(gathered.cpu().numpy(), n_total, world, shards)
     else:
         full = db.download(["summaries"]).summaries
     torch.cuda.synchronize(dev)
@@ -440,7 +451,7 @@ def run_ours(args, rank: int, world: int) -> None:
         t0 = time.perf_counter()
         out = evaluate_scenarios(scenarios, evaluator=ev)
         if world > 1:
-            gather_summaries(out.summaries, n_total, rank, world, device=dev)
+            gather_summaries(out.summaries, n_total, rank, world, device=dev, shards=shards)
         torch.cuda.synchronize(dev)
         if k >= args.warmup:
             e2e_times.append(time.perf_counter() - t0)
@@ -504,7 +515,8 @@ def run_ours(args, rank: int, world: int) -> None:
                 "requests": int(total_req),
                 "events": int(full["n_events"].sum()),
                 "status_counts": {_abi.STATUS_NAMES[i]: int(c) for i, c in enumerate(statuses) if c},
-                "parallelism": f"scenario shards i mod {world}, one all_gather_into_tensor of summaries per step",
+                "parallelism": f"{world} cost-balanced static scenario shards (sorted by estimated device time, "
+                               "dealt round-robin), one all_gather_into_tensor of summaries per step",
                 "l2": "flushed (256 MiB write) between timed steps",
                 "stall_watchdog": engine.STALL_EVENT_LIMIT,
             },

@@ -377,6 +377,25 @@ def compile_batch(scenarios: list[Scenario], stall_limit: int, validate: bool = 
     return CompiledBatch(arrival, inp, outp, recs, table, tix, sizes)
 
 
+def dispatch_estimate(cb: CompiledBatch) -> tuple[np.ndarray, np.ndarray]:
+    """(relative device-time estimate per scenario, per-scenario trace stats
+    [n, first arrival, last arrival, total output]); see dispatch_order."""
+    stats = np.zeros((len(cb.table.entries), 4))     # n, first, last, total output per trace
+    for j, e in enumerate(cb.table.entries):
+        n = entry_len(e)
+        if n < 2:
+            continue
+        if isinstance(e, DeviceTraceEntry):
+            stats[j] = n, e.device.first_arrival, e.device.last_arrival, float(e.device.sum_output)
+        else:
+            stats[j] = n, float(e.arrival[0]), float(e.arrival[-1]), float(e.output_len.sum())
+    tix = np.asarray(cb.trace_index, dtype=np.int64)
+    n, first, last, total_out = (stats[tix, c] for c in range(4))
+    span = (last - first) * cb.scenarios["arrival_scale"]
+    per_inst = (n - 1) / np.maximum(span, 1e-9) / np.maximum(cb.scenarios["n_instances"], 1)
+    return np.where(n >= 2, total_out / (1.0 + per_inst), 0.0), stats[tix]
+
+
 def dispatch_order(cb: CompiledBatch) -> np.ndarray:
     """Dispatch order for the persistent kernel's work queue: scenarios
     grouped by scheduling policy (strategy, flips) and trace, longest-first
@@ -392,20 +411,8 @@ def dispatch_order(cb: CompiledBatch) -> np.ndarray:
     total output tokens divided by the average decode batch, which shrinks as
     the per-instance arrival rate falls.  The order only schedules work;
     results do not depend on it."""
-    stats = np.zeros((len(cb.table.entries), 4))     # n, first, last, total output per trace
-    for j, e in enumerate(cb.table.entries):
-        n = entry_len(e)
-        if n < 2:
-            continue
-        if isinstance(e, DeviceTraceEntry):
-            stats[j] = n, e.device.first_arrival, e.device.last_arrival, float(e.device.sum_output)
-        else:
-            stats[j] = n, float(e.arrival[0]), float(e.arrival[-1]), float(e.output_len.sum())
-    tix = np.asarray(cb.trace_index, dtype=np.int64)
-    n, first, last, total_out = (stats[tix, c] for c in range(4))
-    span = (last - first) * cb.scenarios["arrival_scale"]
-    per_inst = (n - 1) / np.maximum(span, 1e-9) / np.maximum(cb.scenarios["n_instances"], 1)
-    est = np.where(n >= 2, total_out / (1.0 + per_inst), 0.0)
+    est, st = dispatch_estimate(cb)
+    n, first, last, total_out = (st[:, c] for c in range(4))
     policy = cb.scenarios["strategy"].astype(np.int64) * 2 + cb.scenarios["enable_flips"].astype(np.int64)
     # traces grouped by content (equal traces held by distinct objects group together)
     trace = np.unique(np.stack([n, first, last, total_out], axis=1), axis=0, return_inverse=True)[1].reshape(-1)

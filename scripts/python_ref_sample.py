@@ -20,6 +20,8 @@ import sys
 import time
 from pathlib import Path
 
+import numpy as np
+
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
@@ -56,6 +58,23 @@ def main() -> None:
         out["per_config"][cfg] = {"scenarios": len(rs), "requests": req, "events": sum(r["events"] for r in rs),
                                   "python_s": py, "port_s": po, "python_req_per_s_per_core": req / py,
                                   "port_req_per_s_per_core": req / po, "python_over_port": py / po}
+    # whole sweeps run through the real reference by oracle/gen_golden_digest.py
+    # (7 worker processes on the 8-core build container, so per-scenario wall
+    # times include some contention)
+    out["whole_sweeps"] = {}
+    for cfg, total in (("c3", 1920), ("c4", 1080), ("c5", None)):
+        path = ROOT / "tests" / "golden" / f"digest_{cfg}.npz"
+        if not path.exists():
+            continue
+        with np.load(path) as z:
+            wall = z["wall_s"]
+            ids = z["id"]
+            st = z["status"]
+        import paper_2505_11916_b200.workloads as W
+        reqs = sum(len(sc.trace) for sc in getattr(W, cfg)(ids))
+        out["whole_sweeps"][cfg] = {"scenarios": int(len(ids)), "of": total or 98304, "requests": int(reqs),
+                                    "stalled": int((st == 1).sum()), "python_core_s": float(wall.sum()),
+                                    "python_req_per_s_per_core": float(reqs / wall.sum())}
     out["scenarios"] = rows
     path = ROOT / "profiles" / "python_reference_sample.json"
     path.write_text(json.dumps(out, indent=1))

@@ -18,7 +18,8 @@ import torch.multiprocessing as mp
 import harness as H
 from paper_2505_11916_b200 import _abi
 from paper_2505_11916_b200._buffers import OutputSpec
-from paper_2505_11916_b200.sweep import assemble_gathered, gather_summaries, gather_summaries_into, shard, shard_bytes
+from paper_2505_11916_b200.sweep import (assemble_gathered, balanced_shards, gather_summaries, gather_summaries_into,
+                                         shard, shard_bytes)
 
 NAMES = ["small_arrow_2_2", "small_noflip", "rr_small", "fuzz_01", "fuzz_02", "fuzz_07", "fuzz_11"]
 
@@ -38,20 +39,23 @@ def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     items = _items()
-    mine = shard(len(items), rank, world)
     limit = {m["stall_limit"] for m, _ in items}.pop()
-    from paper_2505_11916_b200._compile import compile_batch
+    from paper_2505_11916_b200._compile import compile_batch, dispatch_estimate
 
+    # bench.py's split: cost-balanced shards computed identically on every rank
+    shards = balanced_shards(dispatch_estimate(compile_batch([H.golden_scenario(m, a) for m, a in items], limit))[0],
+                             world)
+    mine = shards[rank]
     cb = compile_batch([H.golden_scenario(*items[i]) for i in mine], limit)
     hb = H.run_oracle(cb, OutputSpec(), threads=1)
-    full = gather_summaries(hb.summaries, len(items), rank, world)
+    full = gather_summaries(hb.summaries, len(items), rank, world, shards=shards)
     # the exact device-side path of bench.py (all_gather_into_tensor of
     # padded byte shards, then assembly in global order)
     local = torch.from_numpy(np.ascontiguousarray(hb.summaries).view(np.uint8).reshape(-1).copy())
     padded = torch.zeros(shard_bytes(len(items), world), dtype=torch.uint8)
     gathered = torch.empty(world * padded.numel(), dtype=torch.uint8)
     gather_summaries_into(local, padded, gathered)
-    full2 = assemble_gathered(gathered.numpy(), len(items), world)
+    full2 = assemble_gathered(gathered.numpy(), len(items), world, shards)
     if rank == 0:
         q.put((full.tobytes(), full2.tobytes()))
     dist.destroy_process_group()
@@ -82,7 +86,30 @@ def test_sharded_sweep_gathers_to_single_process_result():
 
 
 def test_shard_is_a_partition():
+    rng = np.random.default_rng(0)
     for n in (1, 7, 96, 1000):
         for world in (1, 2, 4, 8):
             parts = np.concatenate([shard(n, r, world) for r in range(world)])
             assert sorted(parts.tolist()) == list(range(n))
+            bal = balanced_shards(rng.random(n), world)
+            assert sorted(np.concatenate(bal).tolist()) == list(range(n))
+            assert max(len(b) for b in bal) - min(len(b) for b in bal) <= 1
+
+
+def test_balanced_shards_mix_the_c5_radix():
+    """C5 ids are trace-major: i % 8 would hand each of 8 ranks one trace;
+    the cost-aware deal gives every rank every trace and policy."""
+    from paper_2505_11916_b200 import engine
+    from paper_2505_11916_b200 import workloads as W
+    from paper_2505_11916_b200._compile import compile_batch, dispatch_estimate
+
+    ids = np.arange(0, 98304, 7)
+    cb = compile_batch(W.c5(ids), engine.STALL_EVENT_LIMIT)
+    est = dispatch_estimate(cb)[0]
+    for world in (2, 4, 8):
+        shards = balanced_shards(est, world)
+        loads = np.array([est[s].sum() for s in shards])
+        assert loads.max() / loads.mean() < 1.01
+        for s in shards:
+            assert len(set(ids[s] % 4)) == 4                # every trace
+            assert len(set(cb.scenarios["strategy"][s])) == 2 and len(set(cb.scenarios["enable_flips"][s])) == 2
