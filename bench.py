@@ -361,7 +361,7 @@ def run_ours(args, rank: int, world: int) -> None:
                                              balanced_shards, gather_summaries_into, shard_bytes)
     from paper_2505_11916_b200._compile import dispatch_estimate
 
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
