@@ -28,6 +28,11 @@ constexpr int kThreads = kWarpsPerBlock * 32;
 #define ARROW_TP_BLOCKS 3
 #endif
 constexpr int kMinBlocksThroughput = ARROW_TP_BLOCKS;
+// two instances per lane (N > 32) carry twice the register state
+#ifndef ARROW_TP_BLOCKS_IPL2
+#define ARROW_TP_BLOCKS_IPL2 3
+#endif
+constexpr int kMinBlocksThroughput2 = ARROW_TP_BLOCKS_IPL2;
 constexpr int kLatWarps = ARROW_LAT_WARPS;  // warps per block of the latency build
 
 template <int IPL, int MINB, int WPB>
@@ -86,7 +91,7 @@ cudaError_t slots_for(const arrow_batch_t* b, int* slots, bool* throughput) {
   long long lat = 0, thr = 0;
   if (ipl_of(b) == 2) {
     if ((e = capacity_of<2, 1, kLatWarps>(sms, &lat)) != cudaSuccess) return e;
-    if ((e = capacity_of<2, kMinBlocksThroughput, kWarpsPerBlock>(sms, &thr)) != cudaSuccess) return e;
+    if ((e = capacity_of<2, kMinBlocksThroughput2, kWarpsPerBlock>(sms, &thr)) != cudaSuccess) return e;
   } else {
     if ((e = capacity_of<1, 1, kLatWarps>(sms, &lat)) != cudaSuccess) return e;
     if ((e = capacity_of<1, kMinBlocksThroughput, kWarpsPerBlock>(sms, &thr)) != cudaSuccess) return e;
@@ -141,7 +146,7 @@ int arrow_sim_run(const arrow_batch_t* b, void* workspace, size_t workspace_byte
   const int grid = (slots + wpb - 1) / wpb;
   if (ipl_of(b) == 2) {
     if (tp)
-      arrow_sim_kernel<2, kMinBlocksThroughput, kWarpsPerBlock><<<grid, kThreads, 0, st>>>(*b, ws, L, counter, slots);
+      arrow_sim_kernel<2, kMinBlocksThroughput2, kWarpsPerBlock><<<grid, kThreads, 0, st>>>(*b, ws, L, counter, slots);
     else
       arrow_sim_kernel<2, 1, kLatWarps><<<grid, kLatWarps * 32, 0, st>>>(*b, ws, L, counter, slots);
   } else {
