@@ -1827,6 +1827,9 @@ struct Sim {
     }
     const bool some_safe = w.any(any_safe);
     ns_hi = w.min_u32(ns_hi);
+#ifdef ARROW_PROF
+    if (lane == 0) u().cyc_kind[21] += 1;                 // burst selections attempted
+#endif
     if (!some_safe) return false;
     // limit = min(serial head, non-safe events rounded down to their high word)
     uint64_t lim_k = ~0ull;
@@ -1857,6 +1860,9 @@ struct Sim {
     // both reductions issued back to back (independent), then the test
     const uint32_t n_part = w.add_u32((uint32_t)n_mine);
     t_hi = w.min_u32(t_hi);
+#ifdef ARROW_PROF
+    if (lane == 0) u().cyc_kind[22] += 1;                 // ... past the chain-safe test
+#endif
     if (n_part == 0) return false;
     per = (int)(BURST_POOL / n_part);
     if (per > BURST_MAX) per = BURST_MAX;
@@ -1892,7 +1898,11 @@ struct Sim {
       safe[k] = safe[k] && (st[k].ck < hz.k || (st[k].ck == hz.k && k2 < hz.s));
       run = run || safe[k];
     }
-    return w.any(run);
+    const bool go = w.any(run);
+#ifdef ARROW_PROF
+    if (lane == 0 && go) u().cyc_kind[23] += 1;           // ... that run a burst
+#endif
+    return go;
   }
 
   // Decode-only iteration chain of a chain-safe instance, from its pending

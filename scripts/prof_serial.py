@@ -50,6 +50,7 @@ def main():
         print(f"scenario {k}: {tot / 1e6:.1f}M cycles: {parts}")
     agg = p.sum(0) / cyc.sum()
     print("all:", ", ".join(f"{names[q]} {100 * agg[q]:.1f}%" for q in range(21) if names[q] != "-"))
+    print("burst selections: attempted %d, past chain-safe test %d, ran %d" % tuple(p[:, 21:24].sum(0)))
     cnt = p[:, 24:32].sum(0)
     kinds = ["iter?", "-", "prefill_c", "arrival", "tick", "loud_iter", "migration", "-"]
     tot_cyc = cyc.sum()
