@@ -2501,6 +2501,10 @@ struct Sim {
             bool pushed = false;
             ATRACE("loud inst %d pc %d emit %d pool %d mq %d ma %d frees %d\n", I.id, I.pb_pc, I.pb_emit, pool_of(I.id),
                    I.mq_c, I.mig_active, (int)(I.min_f == I.it - 1 || I.pb_rel));
+#ifdef ARROW_PROF
+            if (!I.pb_emit && !I.pb_pc) u().cyc_kind[25] += 1;   // token-less (silent) loud iterations
+            if (I.pb_pc) u().cyc_kind[31] += 1;                  // PREFILL_COMPLETE-pushing ones
+#endif
             u().n_iters++;
             u().tmp_i[0] = iteration_complete<true>(I, now, completed, pushed);
             u().completed += completed;

@@ -1,6 +1,6 @@
 """Serial-step cycle breakdown by event kind (needs a -DARROW_PROF build).
 
-    ARROW_SIM_LIB=/tmp/libprof.so python scripts/prof_serial.py [c2|c5 [sample]]
+    ARROW_SIM_LIB=/tmp/libprof.so python scripts/prof_serial.py [c2|c5 [sample [trace digit]]]
 
 c5: a seeded sample (default 4 096) of the C5 sweep through the occupancy
 build; also prints the step counts (serial / parallel) and per-kind shares.
@@ -28,6 +28,8 @@ def main():
     if which == "c5":
         n = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
         ids = np.sort(np.random.default_rng(5).choice(98304, size=n, replace=False))
+        if len(sys.argv) > 3:                       # restrict to one trace digit (0..3)
+            ids = ids[ids % 4 == int(sys.argv[3])]
         scen = W.c5(ids)
     else:
         scen = W.c2(trace=W.c2_variant_trace(0))
@@ -51,6 +53,7 @@ def main():
     agg = p.sum(0) / cyc.sum()
     print("all:", ", ".join(f"{names[q]} {100 * agg[q]:.1f}%" for q in range(21) if names[q] != "-"))
     print("burst selections: attempted %d, past chain-safe test %d, ran %d" % tuple(p[:, 21:24].sum(0)))
+    print("loud iterations: silent (no token) %d, PREFILL_COMPLETE-pushing %d" % (p[:, 25].sum(), p[:, 31].sum()))
     cnt = p[:, 24:32].sum(0)
     kinds = ["iter?", "-", "prefill_c", "arrival", "tick", "loud_iter", "migration", "-"]
     tot_cyc = cyc.sum()
