@@ -35,7 +35,16 @@ constexpr int kMinBlocksThroughput = ARROW_TP_BLOCKS;
 constexpr int kMinBlocksThroughput2 = ARROW_TP_BLOCKS_IPL2;
 constexpr int kLatWarps = ARROW_LAT_WARPS;  // warps per block of the latency build
 
-template <int IPL, int MINB, int WPB>
+// LEAN: summaries-only batches (no outmap): every optional-output write
+// compiles out of the event loop (smaller hot code; the occupancy build is
+// instruction-fetch bound).  The audit build keeps one variant.
+#ifdef ARROW_AUDIT
+constexpr bool kLeanBuild = false;
+#else
+constexpr bool kLeanBuild = true;
+#endif
+
+template <int IPL, int MINB, int WPB, bool LEAN>
 __global__ void __launch_bounds__(WPB * 32, MINB) arrow_sim_kernel(const arrow_batch_t batch, char* workspace,
                                                                    arrow::SlotLayout L, int* counter, int n_slots) {
   __shared__ arrow::WarpSmem smem[WPB];
@@ -45,7 +54,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) arrow_sim_kernel(const arrow_b
   const int wid = threadIdx.x >> 5;
   const int slot = blockIdx.x * WPB + wid;
   if (slot >= n_slots) return;
-  arrow::Sim<DevWarp, IPL, (MINB > 1)> sim;   // occupancy build: COMPACT code
+  arrow::Sim<DevWarp, IPL, (MINB > 1), LEAN> sim;   // occupancy build: COMPACT code
   sim.sm = &smem[wid];
   sim.B = &sb;
   sim.L = L;
@@ -72,7 +81,7 @@ template <int IPL, int MINB, int WPB>
 cudaError_t capacity_of(int sms, long long* cap) {
   int per_sm = 0;
   cudaError_t e =
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arrow_sim_kernel<IPL, MINB, WPB>, WPB * 32, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arrow_sim_kernel<IPL, MINB, WPB, false>, WPB * 32, 0);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   *cap = (long long)sms * per_sm * WPB;
@@ -144,17 +153,26 @@ int arrow_sim_run(const arrow_batch_t* b, void* workspace, size_t workspace_byte
   if (e != cudaSuccess) return (int)e;
   const int wpb = tp ? kWarpsPerBlock : kLatWarps;
   const int grid = (slots + wpb - 1) / wpb;
+  const bool lean = kLeanBuild && b->outmap == nullptr;
+#define ARROW_LAUNCH(IPL_, MINB_, WPB_)                                                                  \
+  do {                                                                                                  \
+    if (lean)                                                                                           \
+      arrow_sim_kernel<IPL_, MINB_, WPB_, kLeanBuild><<<grid, (WPB_) * 32, 0, st>>>(*b, ws, L, counter, slots); \
+    else                                                                                                \
+      arrow_sim_kernel<IPL_, MINB_, WPB_, false><<<grid, (WPB_) * 32, 0, st>>>(*b, ws, L, counter, slots);     \
+  } while (0)
   if (ipl_of(b) == 2) {
     if (tp)
-      arrow_sim_kernel<2, kMinBlocksThroughput2, kWarpsPerBlock><<<grid, kThreads, 0, st>>>(*b, ws, L, counter, slots);
+      ARROW_LAUNCH(2, kMinBlocksThroughput2, kWarpsPerBlock);
     else
-      arrow_sim_kernel<2, 1, kLatWarps><<<grid, kLatWarps * 32, 0, st>>>(*b, ws, L, counter, slots);
+      ARROW_LAUNCH(2, 1, kLatWarps);
   } else {
     if (tp)
-      arrow_sim_kernel<1, kMinBlocksThroughput, kWarpsPerBlock><<<grid, kThreads, 0, st>>>(*b, ws, L, counter, slots);
+      ARROW_LAUNCH(1, kMinBlocksThroughput, kWarpsPerBlock);
     else
-      arrow_sim_kernel<1, 1, kLatWarps><<<grid, kLatWarps * 32, 0, st>>>(*b, ws, L, counter, slots);
+      ARROW_LAUNCH(1, 1, kLatWarps);
   }
+#undef ARROW_LAUNCH
   return (int)cudaGetLastError();
 }
 

@@ -323,7 +323,12 @@ AS_HD int imin(int a, int b) { return a < b ? a : b; }
 // fit the instruction caches (C5 ncu: 78 % of stall samples "no
 // instruction"), so repeated call sites are folded into non-unrolled loops.
 // The latency build (1-2 warps per SM) keeps them unrolled.
-template <class W, int IPL, bool COMPACT = false>
+#define HAVE_OM (!LEAN && have_om)
+
+// LEAN: the batch requests no optional outputs (a sweep: summaries only);
+// every per-request / decision / snapshot / iteration-log write and its test
+// compile out of the hot paths.
+template <class W, int IPL, bool COMPACT = false, bool LEAN = false>
 struct Sim {
   W w;
   WarpSmem* sm;
@@ -336,7 +341,7 @@ struct Sim {
   const int32_t* inl;
   const int32_t* outl;
   arrow_outmap_t om;
-  bool have_om;
+  bool have_om;                 // read through HAVE_OM
   Inst st[IPL];
 
   static constexpr int WD = W::WIDTH;
@@ -712,7 +717,7 @@ struct Sim {
     if (ad > 0) {
       int* rr = run_rid(I.id);
       int* rf = run_f(I.id);
-      int32_t* dit = (B->req_decode_iter && have_om && om.req_offset >= 0) ? B->req_decode_iter + om.req_offset
+      int32_t* dit = (B->req_decode_iter && HAVE_OM && om.req_offset >= 0) ? B->req_decode_iter + om.req_offset
                                                                             : (int32_t*)0;
       for (int j = 0; j < ad; j++) {
         int rid = wd[ring(I.wd_h, j, L.qcap)];
@@ -790,7 +795,7 @@ struct Sim {
   template <bool SERIAL>
   AS_HD int iteration_complete(Inst& I, double now, int& completed, bool& pushed) {
     const int cur = I.it - 1;
-    if (B->iterlog && have_om && om.iterlog_offset >= 0) {
+    if (B->iterlog && HAVE_OM && om.iterlog_offset >= 0) {
       if (cur < om.iterlog_stride)
         B->iterlog[om.iterlog_offset + (int64_t)I.id * om.iterlog_stride + cur] = now;
       else if (u().overflow == ARROW_OVF_NONE)
@@ -893,7 +898,7 @@ struct Sim {
                   ((uint64_t)(uint32_t)rid << 32);
     h = (h ^ w2) * 1099511628211ull;
     U.hash = h;
-    if (B->decisions && have_om && om.decision_offset >= 0) {
+    if (B->decisions && HAVE_OM && om.decision_offset >= 0) {
       if (U.n_dec < om.decision_capacity) {
         arrow_decision_t* d = B->decisions + om.decision_offset + U.n_dec;
         d->time = now;
@@ -911,7 +916,7 @@ struct Sim {
   AS_HD void log_dispatch(double now, int kind, int rid, int inst, int branch) {
     lane0([&] {
       log_decision(now, kind, rid, inst, branch);
-      if (have_om && om.req_offset >= 0) {
+      if (HAVE_OM && om.req_offset >= 0) {
         int32_t* out = kind == ARROW_DEC_PREFILL_DISPATCH ? B->req_prefill : B->req_decode;
         if (out) out[om.req_offset + rid] = inst | (branch << 16);
       }
@@ -1380,7 +1385,7 @@ struct Sim {
   }
 
   AS_HD void write_snapshots(double now) {
-    if (!(B->snapshots && have_om && om.snapshot_offset >= 0)) return;
+    if (!(B->snapshots && HAVE_OM && om.snapshot_offset >= 0)) return;
     const int N = sc().n_instances;
     const int64_t base = u().n_snap;
 #pragma unroll
@@ -1476,8 +1481,8 @@ struct Sim {
 
   AS_HD void init_scenario(int s) {
     sid = s;
-    have_om = B->outmap != 0;
-    if (have_om) om = B->outmap[s];
+    have_om = !LEAN && B->outmap != 0;
+    if (HAVE_OM) om = B->outmap[s];
     lane0([&] {
       sm->sc = B->scenarios[s];
       Uniform& U = u();
@@ -1519,7 +1524,7 @@ struct Sim {
     // Per-request state starts as "no token yet" only where it can be
     // observed: per-request outputs of a run that stops early.  A completed
     // run writes every first / last time before summarize() reads them.
-    if (have_om && om.req_offset >= 0) {
+    if (HAVE_OM && om.req_offset >= 0) {
       int32_t* rpf = B->req_prefill;
       int32_t* rdc = B->req_decode;
       int32_t* rdi = B->req_decode_iter;
@@ -1915,7 +1920,7 @@ struct Sim {
     const double b1 = s.b1, b0 = s.b0;
     const int kv_cap = s.kv_capacity;
     const int dcap = imin(s.max_batch, s.chunk_budget);
-    double* ilog = (B->iterlog && have_om && om.iterlog_offset >= 0)
+    double* ilog = (B->iterlog && HAVE_OM && om.iterlog_offset >= 0)
                        ? B->iterlog + om.iterlog_offset + (int64_t)I.id * om.iterlog_stride
                        : (double*)0;
     const int64_t ilog_cap = ilog ? om.iterlog_stride : 0;
@@ -2051,7 +2056,7 @@ struct Sim {
           const int ncur = I.it;
           int* rr = run_rid(I.id);
           int* rf = run_f(I.id);
-          int32_t* dit = (B->req_decode_iter && have_om && om.req_offset >= 0)
+          int32_t* dit = (B->req_decode_iter && HAVE_OM && om.req_offset >= 0)
                              ? B->req_decode_iter + om.req_offset
                              : (int32_t*)0;
           for (int j = 0; j < ad; j++) {
@@ -2564,7 +2569,7 @@ struct Sim {
   }
 
   AS_HD void write_diag() {
-    if (!(B->diag && have_om && om.diag_offset >= 0)) return;
+    if (!(B->diag && HAVE_OM && om.diag_offset >= 0)) return;
 #pragma unroll
     for (int k = 0; k < IPL; k++) {
       const Inst& I = st[k];
@@ -2708,7 +2713,7 @@ struct Sim {
     if (U.status == ARROW_OK && sc().n_requests > 0) summarize(out);
     if (lane == 0 && U.status == ARROW_OK && U.overflow != ARROW_OVF_NONE) out->status = ARROW_BUFFER_OVERFLOW;
     // per-request outputs
-    if (have_om && om.req_offset >= 0) {
+    if (HAVE_OM && om.req_offset >= 0) {
       for (int r = lane; r < sc().n_requests; r += WD) {
         if (B->req_first) B->req_first[om.req_offset + r] = p.first[r];
         if (B->req_last) B->req_last[om.req_offset + r] = p.last[r];
