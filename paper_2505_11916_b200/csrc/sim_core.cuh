@@ -325,6 +325,22 @@ AS_HD int imin(int a, int b) { return a < b ? a : b; }
 // The latency build (1-2 warps per SM) keeps them unrolled.
 #define HAVE_OM (!LEAN && have_om)
 
+#if defined(__CUDA_ARCH__)
+#define AS_NOINL __noinline__
+#else
+#define AS_NOINL __attribute__((noinline))
+#endif
+
+// First error wins (status codes of include/arrow_sim.h).  A free function
+// taking the shared-memory state by pointer, so the out-of-line call does
+// not force the simulator object out of registers.
+AS_NOINL AS_HD void status_set(Uniform* U, int s, int ovf) {
+  if (U->status == ARROW_OK) {
+    U->status = s;
+    if (ovf != ARROW_OVF_NONE) U->overflow = ovf;
+  }
+}
+
 // LEAN: the batch requests no optional outputs (a sweep: summaries only);
 // every per-request / decision / snapshot / iteration-log write and its test
 // compile out of the hot paths.
@@ -387,19 +403,13 @@ struct Sim {
     return w.shfl(v, lane_of(id));
   }
 
-  AS_HD void set_status(int s, int ovf = ARROW_OVF_NONE) {
-    // caller must be a single lane
-    if (u().status == ARROW_OK) {
-      u().status = s;
-      if (ovf != ARROW_OVF_NONE) u().overflow = ovf;
-    }
-  }
+  // caller must be a single lane; out of line (error paths only)
+  AS_HD void set_status(int s, int ovf = ARROW_OVF_NONE) { status_set(&sm->u, s, ovf); }
 
-  AS_HD uint32_t next_seq() {
-    uint32_t s = u().seq++;
-    if (s >= SEQ_LIMIT) set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_SEQ);
-    return s;
-  }
+  // The 2^28 sequence budget (the order key packs kind << 28 | seq) is
+  // checked once per step (serial bookkeeping, rounds, bursts, end of run),
+  // not at every push: a run that exhausts it ends as BUFFER_OVERFLOW.
+  AS_HD uint32_t next_seq() { return u().seq++; }
 
   // ------------------------------------------------------ warp argmin --
 
@@ -2442,6 +2452,7 @@ struct Sim {
       const int ev = h.code;
       double now = tkey_inv(h.k);
       lane0([&] {
+        if (u().seq >= SEQ_LIMIT) set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_SEQ);
         u().now = now;
         u().esp++;
         u().n_events++;
@@ -2551,6 +2562,10 @@ struct Sim {
 #endif
     }
     // end-of-run checks, engine.py:286-290
+    lane0([&] {
+      if (u().seq >= SEQ_LIMIT) set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_SEQ);
+    });
+    if (u().status != ARROW_OK) return;
     const int completed = u().completed;
     w.sync();
     if (completed != sc().n_requests) {
