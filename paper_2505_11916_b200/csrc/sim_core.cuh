@@ -331,6 +331,28 @@ AS_HD int imin(int a, int b) { return a < b ? a : b; }
 #define AS_NOINL __attribute__((noinline))
 #endif
 
+// The waiting-prefill part of predicted_prefill_delay (instance.py:318-321):
+// d += term for each waiting prompt, in queue order (a left fold), from the
+// ring of cached predictor terms.  Out of line: the exact fold is the rare
+// fallback of the delay intervals, and inlined it cost one unrolled copy per
+// call site.
+AS_NOINL AS_HD double delay_fold(double d, const double* t, int h, int c, int cap) {
+  int j = 0;
+  for (; j + 4 <= c; j += 4) {
+    const int a = h + j >= cap ? h + j - cap : h + j;
+    const int b = a + 1 >= cap ? a + 1 - cap : a + 1;
+    const int e = b + 1 >= cap ? b + 1 - cap : b + 1;
+    const int f = e + 1 >= cap ? e + 1 - cap : e + 1;
+    const double t0 = t[a], t1 = t[b], t2 = t[e], t3 = t[f];
+    d += t0;
+    d += t1;
+    d += t2;
+    d += t3;
+  }
+  for (; j < c; j++) d += t[h + j >= cap ? h + j - cap : h + j];
+  return d;
+}
+
 // First error wins (status codes of include/arrow_sim.h).  A free function
 // taking the shared-memory state by pointer, so the out-of-line call does
 // not force the simulator object out of registers.
@@ -487,21 +509,7 @@ struct Sim {
       d += (0.0 > x) ? 0.0 : x;
     }
     if (I.rp_rid >= 0) d += quad(s.pred_a2, s.pred_a1, s.pred_a0, inl[I.rp_rid] - I.rp_done);
-    const double* t = wp_term(I.id);
-    int h = I.wp_h;
-    int c = I.wp_c;
-    int64_t cap = L.qcap;
-    int j = 0;
-    for (; j + 4 <= c; j += 4) {
-      double t0 = t[ring(h, j, cap)], t1 = t[ring(h, j + 1, cap)];
-      double t2 = t[ring(h, j + 2, cap)], t3 = t[ring(h, j + 3, cap)];
-      d += t0;
-      d += t1;
-      d += t2;
-      d += t3;
-    }
-    for (; j < c; j++) d += t[ring(h, j, cap)];
-    return d;
+    return I.wp_c ? delay_fold(d, wp_term(I.id), I.wp_h, I.wp_c, (int)L.qcap) : d;
   }
 
   // Double-double accumulate (hi, lo) += t (Knuth two-sum; no contraction).
