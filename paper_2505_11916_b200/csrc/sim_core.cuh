@@ -897,11 +897,10 @@ struct Sim {
       dst = P_DECODE;
     else if (pk == P_D2P && !has_decode_work(I))
       dst = P_PREFILL;
-    if (SERIAL) {
-      if (nd + npf > 0) u().esp = 0;   // _start_migrations + _kick follow in serial_tail()
-    } else {
-      pushed = kick(I, now);
-    }
+    if (SERIAL && nd + npf > 0) u().esp = 0;
+    // _start_migrations (serial path) and _kick follow in simulate(): one
+    // shared kick site for the serial and the lane-parallel paths
+    (void)pushed;
     return dst;
   }
 
@@ -1379,26 +1378,39 @@ struct Sim {
   // order (engine.py:211-223, 228-236, 240-248), from one code site: each
   // inlined copy of kick() is ~300 instructions, and the occupancy build's
   // hot loop does not fit the instruction cache as it is.
-  AS_HD void serial_tail(int m0, int m1, int k0, int k1, double now) {
+  // The serial handlers' trailing _start_migrations (in program order, each
+  // push sequenced at once); their _kick calls run in the shared kick phase.
+  AS_HD void serial_migs(int m0, int m1, double now) {
     if (u().status != ARROW_OK) return;
-    auto step = [&](int q) {
-      const int id = q == 0 ? m0 : q == 1 ? m1 : q == 2 ? k0 : k1;
-      if (id < 0) return;
-      const bool mig = q < 2;
-      owner(id, [&](Inst& I) {
-        if (mig) {
-          if (start_mig(I, now)) I.mig_seq = next_seq();
-        } else if (kick(I, now)) {
-          I.iter_seq = next_seq();
-        }
-      });
-    };
-    if constexpr (COMPACT) {
 #pragma unroll 1
-      for (int q = 0; q < 4; q++) step(q);
-    } else {
+    for (int q = 0; q < 2; q++) {
+      const int id = q == 0 ? m0 : m1;
+      if (id < 0) continue;
+      owner(id, [&](Inst& I) {
+        if (start_mig(I, now)) I.mig_seq = next_seq();
+      });
+    }
+  }
+
+  // The one inlined copy of kick(): every lane with want[k] starts its
+  // instance's next iteration at tnow[k] (engine.py:170-177).
+  AS_HD void kick_phase(const bool want[IPL], const double tnow[IPL], bool pushed[IPL]) {
 #pragma unroll
-      for (int q = 0; q < 4; q++) step(q);
+    for (int k = 0; k < IPL; k++) pushed[k] = want[k] && kick(st[k], tnow[k]);
+  }
+
+  // Serial kicks sequenced in program order (k0 before k1).
+  AS_HD void serial_kick_seqs(int k0, int k1, const bool pushed[IPL]) {
+#pragma unroll 1
+    for (int q = 0; q < 2; q++) {
+      const int id = q == 0 ? k0 : k1;
+      if (id < 0) continue;
+      if (lane == lane_of(id)) {
+#pragma unroll
+        for (int k = 0; k < IPL; k++)
+          if (st[k].id == id && pushed[k]) st[k].iter_seq = next_seq();
+      }
+      w.sync();
     }
   }
 
@@ -1709,27 +1721,29 @@ struct Sim {
 
   // One parallel round of quiet iteration completions; folds any loud
   // event the round created into the head.
-  AS_HD void run_round(const bool part[IPL], Head& h) {
-    uint64_t key1[IPL];
-    uint32_t key2[IPL];
-    bool pushed[IPL];
-    int completed = 0, n_part = 0;
-    PROF_CLOCK(pr0);
+  // Lane-parallel round, part 1: the participants' completions (their
+  // kicks follow in the shared kick phase, then round_finish()).
+  AS_HD void round_complete(const bool part[IPL], uint64_t key1[IPL], uint32_t key2[IPL], double tnow[IPL],
+                            int& completed, int& n_part) {
 #pragma unroll
     for (int k = 0; k < IPL; k++) {
-      pushed[k] = false;
       key1[k] = 0;
       key2[k] = 0;
+      tnow[k] = 0.0;
       if (!part[k]) continue;
       Inst& I = st[k];
       key1[k] = tkey(I.busy_until);
       key2[k] = I.iter_seq;
+      tnow[k] = I.busy_until;
       n_part++;
-      iteration_complete<false>(I, I.busy_until, completed, pushed[k]);
+      bool unused = false;
+      iteration_complete<false>(I, I.busy_until, completed, unused);
     }
-#ifdef ARROW_PROF
-    w.sync();
-#endif
+  }
+
+  AS_HD void round_finish(const bool part[IPL], const uint64_t key1[IPL], const uint32_t key2[IPL],
+                          const bool pushed[IPL], int completed, int n_part, Head& h) {
+    PROF_CLOCK(pr0);
     PROF_MARK(0, pr0);
     PROF_CLOCK(pr1);
     // exact push sequence: the round's pushes, in (time, seq) order of the
@@ -2427,6 +2441,19 @@ struct Sim {
       bool cand[IPL];
       Head hz;
       int per = 0;
+      // shared kick phase inputs: a lane-parallel round's participants, or the
+      // serial handler's kick targets (tk0 before tk1)
+      bool round = false;
+      bool want[IPL];
+      double tnow[IPL];
+      uint64_t key1[IPL];
+      uint32_t key2[IPL];
+      int completed = 0, n_part = 0;
+      int tk0 = -1, tk1 = -1;
+      double now = 0.0;
+#ifdef ARROW_PROF
+      int prof_kind = 0;
+#endif
       PROF_CLOCK(c0);
       if (round_candidates(h, cand)) {
         const bool bsel = burst_select(h, hz, part, per);
@@ -2445,20 +2472,15 @@ struct Sim {
         PROF_CLOCK(cr);
         round_select(cand, part);
         PROF_MARK(10, cr);
-        PROF_CLOCK(cx);
-        run_round(part, h);
-        AUDIT_STEP();
-        PROF_MARK(11, cx);
-        PROF_ADD(cyc_round, c0);
-        const int status = u().status;
-        w.sync();
-        if (status != ARROW_OK) return;
-        continue;
-      }
+        round = true;
+        round_complete(part, key1, key2, tnow, completed, n_part);
+#pragma unroll
+        for (int k = 0; k < IPL; k++) want[k] = part[k];
+      } else {
       PROF_MARK(8, c0);
       if (h.code < 0) break;
       const int ev = h.code;
-      double now = tkey_inv(h.k);
+      now = tkey_inv(h.k);
       lane0([&] {
         if (u().seq >= SEQ_LIMIT) set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_SEQ);
         u().now = now;
@@ -2468,11 +2490,11 @@ struct Sim {
         ATRACE("ev %d t=%.17g esp=%lld\n", ev, now, (long long)u().esp);
       });
 #ifdef ARROW_PROF
-      const int prof_kind = ev >= 1000 ? ev - 1000 : ((ev & 1) ? 5 : 6);
+      prof_kind = ev >= 1000 ? ev - 1000 : ((ev & 1) ? 5 : 6);
       if (lane == 0) u().cyc_kind[24 + prof_kind] += 1;   // event counts by kind
       PROF_MARK(20, c0);                                   // selection + bookkeeping up to here
 #endif
-      int tm0 = -1, tm1 = -1, tk0 = -1, tk1 = -1;   // serial_tail() arguments
+      int tm0 = -1, tm1 = -1;   // serial_migs() arguments
       if (ev >= 1000) {
         int kind = ev - 1000;
         if (kind == EV_ARRIVAL) {
@@ -2544,9 +2566,30 @@ struct Sim {
           tm1 = tk1 = src;
         }
       }
+      serial_migs(tm0, tm1, now);
+      const bool ok = u().status == ARROW_OK;
+#pragma unroll
+      for (int k = 0; k < IPL; k++) {
+        want[k] = ok && st[k].id >= 0 && (st[k].id == tk0 || st[k].id == tk1);
+        tnow[k] = now;
+      }
+      }   // serial step
+      bool pushed[IPL];
       PROF_CLOCK(pt0);
-      serial_tail(tm0, tm1, tk0, tk1, now);
+      kick_phase(want, tnow, pushed);       // the one inlined copy of kick()
       PROF_MARK(18, pt0);
+      if (round) {
+        PROF_CLOCK(cx);
+        round_finish(part, key1, key2, pushed, completed, n_part, h);
+        AUDIT_STEP();
+        PROF_MARK(11, cx);
+        PROF_ADD(cyc_round, c0);
+        const int status = u().status;
+        w.sync();
+        if (status != ARROW_OK) return;
+        continue;
+      }
+      serial_kick_seqs(tk0, tk1, pushed);
       AUDIT_STEP();
       const int status = u().status;
       const int64_t esp = u().esp;
