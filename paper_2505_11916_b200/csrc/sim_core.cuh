@@ -810,8 +810,7 @@ struct Sim {
   // `completed`; returns the drained-pool move (-1 none); sets `pushed` when
   // the next iteration started (non-SERIAL: lane-parallel rounds; the serial
   // path starts migrations and kicks in serial_tail()).
-  template <bool SERIAL>
-  AS_HD int iteration_complete(Inst& I, double now, int& completed, bool& pushed) {
+  AS_HD int iteration_complete(Inst& I, double now, int& completed, bool serial) {
     const int cur = I.it - 1;
     if (B->iterlog && HAVE_OM && om.iterlog_offset >= 0) {
       if (cur < om.iterlog_stride)
@@ -897,10 +896,9 @@ struct Sim {
       dst = P_DECODE;
     else if (pk == P_D2P && !has_decode_work(I))
       dst = P_PREFILL;
-    if (SERIAL && nd + npf > 0) u().esp = 0;
+    if (serial && nd + npf > 0) u().esp = 0;
     // _start_migrations (serial path) and _kick follow in simulate(): one
     // shared kick site for the serial and the lane-parallel paths
-    (void)pushed;
     return dst;
   }
 
@@ -1723,8 +1721,11 @@ struct Sim {
   // event the round created into the head.
   // Lane-parallel round, part 1: the participants' completions (their
   // kicks follow in the shared kick phase, then round_finish()).
+  // serial: the loud ITERATION_COMPLETE of one instance (its owner lane is
+  // the only participant): one inlined copy of iteration_complete() serves
+  // both paths.
   AS_HD void round_complete(const bool part[IPL], uint64_t key1[IPL], uint32_t key2[IPL], double tnow[IPL],
-                            int& completed, int& n_part) {
+                            int& completed, int& n_part, bool serial) {
 #pragma unroll
     for (int k = 0; k < IPL; k++) {
       key1[k] = 0;
@@ -1736,9 +1737,24 @@ struct Sim {
       key2[k] = I.iter_seq;
       tnow[k] = I.busy_until;
       n_part++;
-      bool unused = false;
-      iteration_complete<false>(I, I.busy_until, completed, unused);
+      if (serial) {
+        ATRACE("loud inst %d pc %d emit %d pool %d mq %d ma %d frees %d\n", I.id, I.pb_pc, I.pb_emit, pool_of(I.id),
+               I.mq_c, I.mig_active, (int)(I.min_f == I.it - 1 || I.pb_rel));
+#ifdef ARROW_PROF
+        if (!I.pb_emit && !I.pb_pc) u().cyc_kind[25] += 1;   // token-less (silent) loud iterations
+        if (I.pb_pc) u().cyc_kind[31] += 1;                  // PREFILL_COMPLETE-pushing ones
+#endif
+      }
+      int done = 0;
+      const int dst = iteration_complete(I, I.busy_until, done, serial);
+      completed += done;
+      if (serial) {
+        u().n_iters++;
+        u().tmp_i[0] = dst;
+        u().completed += done;
+      }
     }
+    if (serial) w.sync();
   }
 
   AS_HD void round_finish(const bool part[IPL], const uint64_t key1[IPL], const uint32_t key2[IPL],
@@ -2450,6 +2466,7 @@ struct Sim {
       uint32_t key2[IPL];
       int completed = 0, n_part = 0;
       int tk0 = -1, tk1 = -1;
+      int iter_id = -1, serial_tm0 = -1, serial_tm1 = -1;
       double now = 0.0;
 #ifdef ARROW_PROF
       int prof_kind = 0;
@@ -2473,9 +2490,6 @@ struct Sim {
         round_select(cand, part);
         PROF_MARK(10, cr);
         round = true;
-        round_complete(part, key1, key2, tnow, completed, n_part);
-#pragma unroll
-        for (int k = 0; k < IPL; k++) want[k] = part[k];
       } else {
       PROF_MARK(8, c0);
       if (h.code < 0) break;
@@ -2540,31 +2554,33 @@ struct Sim {
       } else {
         int id = ev >> 1;
         if (ev & 1) {
-          int dst = -1;
-          PROF_CLOCK(pi0);
-          owner(id, [&](Inst& I) {
-            int completed = 0;
-            bool pushed = false;
-            ATRACE("loud inst %d pc %d emit %d pool %d mq %d ma %d frees %d\n", I.id, I.pb_pc, I.pb_emit, pool_of(I.id),
-                   I.mq_c, I.mig_active, (int)(I.min_f == I.it - 1 || I.pb_rel));
-#ifdef ARROW_PROF
-            if (!I.pb_emit && !I.pb_pc) u().cyc_kind[25] += 1;   // token-less (silent) loud iterations
-            if (I.pb_pc) u().cyc_kind[31] += 1;                  // PREFILL_COMPLETE-pushing ones
-#endif
-            u().n_iters++;
-            u().tmp_i[0] = iteration_complete<true>(I, now, completed, pushed);
-            u().completed += completed;
-          });
-          dst = u().tmp_i[0];
-          w.sync();
-          PROF_MARK(19, pi0);
-          if (dst >= 0) move_and_log(id, dst, now, ARROW_TRIG_DRAINED);
-          tm0 = tk0 = id;
+          iter_id = id;               // the ITERATION_COMPLETE handler runs in round_complete() below
+#pragma unroll
+          for (int k = 0; k < IPL; k++) part[k] = st[k].id == id;
         } else {
           const int src = on_migration_complete(id, now);
           tm0 = tk0 = id;
           tm1 = tk1 = src;
         }
+      }
+      serial_tm0 = tm0;
+      serial_tm1 = tm1;
+      }   // serial step (handlers)
+      if (round || iter_id >= 0) {
+        PROF_CLOCK(pi0);
+        round_complete(part, key1, key2, tnow, completed, n_part, !round);
+        PROF_MARK(19, pi0);
+      }
+      if (round) {
+#pragma unroll
+        for (int k = 0; k < IPL; k++) want[k] = part[k];
+      } else {
+      int tm0 = serial_tm0, tm1 = serial_tm1;
+      if (iter_id >= 0) {           // engine.py:219-223: drained move, then migrations and the kick
+        const int dst = u().tmp_i[0];
+        w.sync();
+        if (dst >= 0) move_and_log(iter_id, dst, now, ARROW_TRIG_DRAINED);
+        tm0 = tk0 = iter_id;
       }
       serial_migs(tm0, tm1, now);
       const bool ok = u().status == ARROW_OK;
