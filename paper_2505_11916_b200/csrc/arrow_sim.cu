@@ -17,7 +17,10 @@ namespace {
 #ifndef ARROW_LAT_WARPS
 #define ARROW_LAT_WARPS 2
 #endif
-constexpr int kWarpsPerBlock = 4;
+#ifndef ARROW_TP_WARPS
+#define ARROW_TP_WARPS 4
+#endif
+constexpr int kWarpsPerBlock = ARROW_TP_WARPS;
 constexpr int kThreads = kWarpsPerBlock * 32;
 // Two builds of the kernel: MINB = 1 lets the compiler use every register it
 // wants (shortest per-scenario chains: a sweep that fits in one wave of

@@ -292,6 +292,20 @@ AS_HD double quad(double a2, double a1, double a0, int len) {
 
 AS_HD int imin(int a, int b) { return a < b ? a : b; }
 
+// min(BURST_POOL / n, BURST_MAX) for 1 <= n <= 64 without an integer
+// division (a ~20-instruction sequence): 512/n is an integer or at least 1/64
+// away from one, far more than __fdividef's 2-ulp error, so floor(q + 1/1024)
+// is exact.
+AS_HD int burst_share(uint32_t n) {
+  static_assert(BURST_POOL == 512 && BURST_MAX == 64, "burst_share assumes 512 / 64");
+  if (n <= 8) return BURST_MAX;
+#ifdef __CUDA_ARCH__
+  return __float2int_rz(__fdividef(512.0f, (float)n) + 0x1p-10f);
+#else
+  return (int)(BURST_POOL / n);
+#endif
+}
+
 // ------------------------------------------------------------- simulator --
 
 #ifdef ARROW_PROF
@@ -1917,8 +1931,7 @@ struct Sim {
     if (lane == 0) u().cyc_kind[22] += 1;                 // ... past the chain-safe test
 #endif
     if (n_part == 0) return false;
-    per = (int)(BURST_POOL / n_part);
-    if (per > BURST_MAX) per = BURST_MAX;
+    per = burst_share(n_part);
     // at most `per` events per instance: decode-only iterations last >= b1 + b0
     // (t0 <= the earliest participant's time)
     const double t0 = tkey_inv((uint64_t)t_hi << 32);
