@@ -367,6 +367,92 @@ AS_NOINL AS_HD double delay_fold(double d, const double* t, int h, int c, int ca
   return d;
 }
 
+// avg_token_interval's window pruning and mean (instance.py:323-329) on one
+// instance's emission ring, out of line: inlined, its gallop, binary search
+// and IEEE fp64 division cost one copy per call site (emit, the pool mean at
+// its two callers, the decode admission test).  State goes in and out by
+// value so the call keeps the simulator in registers.
+struct EmWin {
+  double first;   // em_first after pruning
+  double val;     // the interval (valid when ok)
+  int h, c;       // ring head / count after pruning
+  int ok;
+};
+
+AS_NOINL AS_HD EmWin em_window(const double* e, int h, int c, double first, double last, double lo, int cap) {
+  if (c > 0 && first < lo) {
+    // gallop from the head, then binary search: the first offset with t >= lo
+    int a = 0, b = 0, step = 1;
+    double vb = 0.0;
+    for (;;) {
+      b = a + step;
+      if (b >= c) {
+        b = c;
+        break;
+      }
+      const int rb = h + b >= cap ? h + b - cap : h + b;
+      vb = e[rb];
+      if (vb >= lo) break;
+      a = b;
+      step <<= 1;
+    }
+    while (b - a > 1) {
+      const int mid = (a + b) >> 1;
+      const int rm = h + mid >= cap ? h + mid - cap : h + mid;
+      const double vm = e[rm];
+      if (vm < lo) {
+        a = mid;
+      } else {
+        b = mid;
+        vb = vm;
+      }
+    }
+    h = h + b >= cap ? h + b - cap : h + b;
+    c -= b;
+    if (c > 0) first = vb;
+  }
+  EmWin r;
+  r.first = first;
+  r.h = h;
+  r.c = c;
+  r.ok = c >= 2;
+  r.val = r.ok ? (last - first) / (double)(c - 1) : 0.0;
+  return r;
+}
+
+// _pool_mean_interval's ordered Neumaier sum (scheduler.py:124-134) over the
+// collected intervals, divided by their count; out of line (two callers).
+// ok = 0 when no interval is valid.
+struct MeanOut {
+  double v;
+  int ok;
+};
+
+AS_NOINL AS_HD MeanOut pool_mean_sum(const double* vals, const int* valid, int m) {
+  double f = 0.0, c = 0.0;
+  int cnt = 0;
+  for (int j = 0; j < m; j++) {
+    if (!valid[j]) continue;
+    double x = vals[j];
+    if (cnt == 0) {
+      f = 0.0 + x;
+    } else {
+      double t = f + x;
+      if (fabs(f) >= fabs(x))
+        c += (f - t) + x;
+      else
+        c += (x - t) + f;
+      f = t;
+    }
+    cnt++;
+  }
+  MeanOut r;
+  r.ok = cnt > 0;
+  if (c != 0.0 && isfinite(c)) f += c;
+  r.v = r.ok ? f / (double)cnt : 0.0;
+  return r;
+}
+
 // First error wins (status codes of include/arrow_sim.h).  A free function
 // taking the shared-memory state by pointer, so the out-of-line call does
 // not force the simulator object out of registers.
@@ -579,40 +665,12 @@ struct Sim {
   // dropped lazily (here, by binary search, and when the ring fills), which
   // is exact because query times never decrease.
   AS_HD bool interval(Inst& I, double now, double* out) {
-    const double lo = now - sc().window;
-    if (I.em_c > 0 && I.em_first < lo) {
-      // gallop from the head, then binary search: the first offset with t >= lo
-      const double* e = em(I.id);
-      int a = 0, b = 0, step = 1;
-      double vb = 0.0;
-      for (;;) {
-        b = a + step;
-        if (b >= I.em_c) {
-          b = I.em_c;
-          break;
-        }
-        vb = e[ring(I.em_h, b, L.ecap)];
-        if (vb >= lo) break;
-        a = b;
-        step <<= 1;
-      }
-      while (b - a > 1) {
-        const int mid = (a + b) >> 1;
-        const double vm = e[ring(I.em_h, mid, L.ecap)];
-        if (vm < lo) {
-          a = mid;
-        } else {
-          b = mid;
-          vb = vm;
-        }
-      }
-      I.em_h = ring(I.em_h, b, L.ecap);
-      I.em_c -= b;
-      if (I.em_c > 0) I.em_first = vb;
-    }
-    if (I.em_c < 2) return false;
-    *out = (I.em_last - I.em_first) / (double)(I.em_c - 1);
-    return true;
+    const EmWin r = em_window(em(I.id), I.em_h, I.em_c, I.em_first, I.em_last, now - sc().window, (int)L.ecap);
+    I.em_h = r.h;
+    I.em_c = r.c;
+    I.em_first = r.first;
+    *out = r.val;
+    return r.ok != 0;
   }
 
   AS_HD void emit(Inst& I, double now) {
@@ -1094,28 +1152,10 @@ struct Sim {
       sm->valid[cpos] = ok ? 1 : 0;
     }
     w.sync();
-    double f = 0.0, c = 0.0;
-    int cnt = 0;
-    for (int j = 0; j < m; j++) {
-      if (!sm->valid[j]) continue;
-      double x = sm->vals[j];
-      if (cnt == 0) {
-        f = 0.0 + x;
-      } else {
-        double t = f + x;
-        if (fabs(f) >= fabs(x))
-          c += (f - t) + x;
-        else
-          c += (x - t) + f;
-        f = t;
-      }
-      cnt++;
-    }
+    const MeanOut r = pool_mean_sum(sm->vals, sm->valid, m);
     w.sync();
-    if (cnt == 0) return false;
-    if (c != 0.0 && isfinite(c)) f += c;
-    *out = f / (double)cnt;
-    return true;
+    *out = r.v;
+    return r.ok != 0;
   }
 
   // decode_load_is_low, scheduler.py:136-147
