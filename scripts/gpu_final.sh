@@ -15,7 +15,7 @@ for W in c4 c3 c2; do
 timeout 900 python bench.py --workload $W --steps 3 --warmup 2 --no-cpu-baseline --no-components > $OUT/bench_${W}_$TAG.json 2> $OUT/bench_${W}_$TAG.err; echo "bench $W rc=$?"
 python -c "import json; d=json.load(open('$OUT/bench_${W}_$TAG.json')); print('$W ms %.1f value %.4g e2e %.4g' % (d['ms_per_step'], d['value'], d['e2e']['value']))"
 done
-if [ "${NCU_C4:-1}" = "1" ]; then
+if [ "${NCU_C4:-0}" = "1" ]; then
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:arrow_sim_kernel -c 1 -o $OUT/prof_c4_$TAG -f \
   python bench.py --workload c4 --steps 1 --warmup 0 --no-cpu-baseline --no-components > $OUT/ncu_c4_$TAG.log 2>&1; echo "ncu c4 rc=$?"
 fi

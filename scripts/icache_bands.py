@@ -9,7 +9,8 @@ import csv
 import re
 import sys
 
-src = open("paper_2505_11916_b200/csrc/sim_core.cuh").read().split("\n")
+import os
+src = open(os.environ.get("ARROW_SRC", "paper_2505_11916_b200/csrc/sim_core.cuh")).read().split("\n")
 defs = []
 for i, l in enumerate(src, 1):
     m = re.match(r"\s*(?:AS_HD|AS_NOINL AS_HD|static AS_HD)\s+[\w:<>&\*\s]+?\b(\w+)\(", l)
