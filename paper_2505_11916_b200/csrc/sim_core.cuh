@@ -73,8 +73,14 @@ static constexpr int MAX_INST = 64;
 #define ARROW_DELAY_SLACK 0x1p-52  // per-term slack of the delay interval (tests widen it to force exact folds)
 #endif
 static constexpr uint32_t SEQ_LIMIT = 1u << 28;
-static constexpr int BURST_POOL = 512;  // chain-burst event keys per warp (shared memory)
-static constexpr int BURST_MAX = 64;    // events per instance per chain burst
+#ifndef ARROW_BURST_POOL
+#define ARROW_BURST_POOL 512
+#endif
+#ifndef ARROW_BURST_MAX
+#define ARROW_BURST_MAX 128
+#endif
+static constexpr int BURST_POOL = ARROW_BURST_POOL;  // chain-burst event keys per warp (shared memory)
+static constexpr int BURST_MAX = ARROW_BURST_MAX;    // events per instance per chain burst
 
 // ---------------------------------------------------------------- layout --
 
@@ -293,14 +299,14 @@ AS_HD double quad(double a2, double a1, double a0, int len) {
 AS_HD int imin(int a, int b) { return a < b ? a : b; }
 
 // min(BURST_POOL / n, BURST_MAX) for 1 <= n <= 64 without an integer
-// division (a ~20-instruction sequence): 512/n is an integer or at least 1/64
-// away from one, far more than __fdividef's 2-ulp error, so floor(q + 1/1024)
-// is exact.
+// division (a ~20-instruction sequence): POOL/n is an integer or at least 1/64
+// away from one, far more than __fdividef's 2-ulp error (POOL <= 2^14), so
+// floor(q + 1/1024) is exact.
 AS_HD int burst_share(uint32_t n) {
-  static_assert(BURST_POOL == 512 && BURST_MAX == 64, "burst_share assumes 512 / 64");
-  if (n <= 8) return BURST_MAX;
+  static_assert(BURST_POOL <= (1 << 14) && BURST_POOL % BURST_MAX == 0, "burst_share bounds");
+  if (n <= (uint32_t)(BURST_POOL / BURST_MAX)) return BURST_MAX;
 #ifdef __CUDA_ARCH__
-  return __float2int_rz(__fdividef(512.0f, (float)n) + 0x1p-10f);
+  return __float2int_rz(__fdividef((float)BURST_POOL, (float)n) + 0x1p-10f);
 #else
   return (int)(BURST_POOL / n);
 #endif
