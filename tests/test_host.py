@@ -145,8 +145,8 @@ def test_percentile_and_max_rate():
 def test_emission_ring_bound_covers_window():
     cfg = arrow.default_run_config()
     cap = emission_capacity(cfg)
-    # twice the window of 5 s / shortest iteration (b1 + b0 = 5.02 ms): 2 x ~1000 emissions
-    assert 1980 < cap < 2200
+    # four windows of 5 s / shortest iteration (b1 + b0 = 5.02 ms): 4 x ~1000 emissions
+    assert 3960 < cap < 4400
     assert emission_capacity(arrow.config_from_values({**arrow.config.DEFAULTS, "a0": 0.0, "a1": 0.0, "a2": 0.0})) \
         == 1 << 16
 
