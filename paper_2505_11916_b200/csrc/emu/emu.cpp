@@ -100,6 +100,7 @@ struct EmuWarp {
     sync();
     return m;
   }
+  uint32_t match_any_u32(uint32_t v) const { return match_any((uint64_t)v); }
   int atomic_add_shared(int* p, int v) const { return __atomic_fetch_add(p, v, __ATOMIC_RELAXED); }
 };
 

@@ -2283,9 +2283,13 @@ struct Sim {
       // event time is distinct (one match), lane order is as good as rank
       // order and the merge is two votes.
       const bool fin = safe[0] && lastp[0];
-      const uint64_t nk = fin ? tkey(st[0].busy_until) : (uint64_t)lane;  // dummies: sign bit clear
-      const uint32_t peers = w.match_any(nk);
       const uint32_t fm = w.ballot(fin);
+      // a 32-bit fold of the pushed time key (match.any on 32 bits is cheaper
+      // than on 64): equal keys fold equal; distinct keys that happen to
+      // collide only send the burst down the exact merge below
+      const uint64_t nk = tkey(st[0].busy_until);
+      const uint32_t hv = fin ? ((uint32_t)nk ^ ((uint32_t)(nk >> 32) * 0x9E3779B1u)) : 0u;
+      const uint32_t peers = w.match_any_u32(hv) & fm;
       const bool dup = w.any(fin && (peers & (peers - 1u)) != 0);
       if (!dup) {
         const uint32_t packed = w.add_u32((uint32_t)events | ((uint32_t)completed << 16));

@@ -32,6 +32,7 @@ struct DevWarp {
   AS_DEV uint32_t max_u32(uint32_t v) const { return __reduce_max_sync(FULL, v); }
   AS_DEV uint32_t add_u32(uint32_t v) const { return __reduce_add_sync(FULL, v); }
   AS_DEV uint32_t match_any(uint64_t v) const { return __match_any_sync(FULL, v); }
+  AS_DEV uint32_t match_any_u32(uint32_t v) const { return __match_any_sync(FULL, v); }
   AS_DEV int atomic_add_shared(int* p, int v) const { return atomicAdd(p, v); }
 };
 #endif
