@@ -2234,8 +2234,8 @@ struct Sim {
   AS_HD void run_burst(const bool safe[IPL], const Head& hz, int per, Head& h) {
     // segments: participant rank (slot-major, then lane) x per
     int rank[IPL];
+    int base_rank = 0;      // after the loop: the number of participants
     {
-      int base_rank = 0;
 #pragma unroll
       for (int kk = 0; kk < IPL; kk++) {
         const uint32_t m = w.ballot(safe[kk]);
@@ -2293,7 +2293,9 @@ struct Sim {
       const bool dup = w.any(fin && (peers & (peers - 1u)) != 0);
       if (!dup) {
         const uint32_t packed = w.add_u32((uint32_t)events | ((uint32_t)completed << 16));
-        const uint32_t total_push = w.add_u32((uint32_t)pushes);
+        // every chain pushes after each event but possibly its last:
+        // pushes = events - participants + finals (no second reduction)
+        const uint32_t total_push = (packed & 0xffffu) - (uint32_t)base_rank + (uint32_t)popc32(fm);
         if (fin) st[0].iter_seq = base + total_push - (uint32_t)popc32(fm) + (uint32_t)popc32(fm & ((1u << lane) - 1u));
         PROF_MARK(13, pb1);
         burst_finish(safe, base, packed, total_push, h);
