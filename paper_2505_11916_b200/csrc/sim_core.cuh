@@ -385,11 +385,42 @@ struct EmWin {
   int ok;
 };
 
+// PROBE: start the search at the interpolated offset (emission times are
+// close to evenly spaced; only the search start depends on it, never the
+// result).  Used by the two-instances-per-lane build (C4 -4.5 %); the
+// one-instance builds keep exactly the plain gallop (C5 +0.7 % with it).
+template <bool PROBE>
 AS_NOINL AS_HD EmWin em_window(const double* e, int h, int c, double first, double last, double lo, int cap) {
   if (c > 0 && first < lo) {
     // gallop from the head, then binary search: the first offset with t >= lo
     int a = 0, b = 0, step = 1;
     double vb = 0.0;
+    if (PROBE && c > 16 && last >= lo) {
+#ifdef __CUDA_ARCH__
+      int g = __float2int_rz(__fdividef((float)(lo - first), (float)(last - first)) * (float)(c - 1));
+#else
+      int g = (int)((float)(lo - first) / (float)(last - first) * (float)(c - 1));
+#endif
+      g = g < 1 ? 1 : (g > c - 1 ? c - 1 : g);
+      const int rg = h + g >= cap ? h + g - cap : h + g;
+      const double vg = e[rg];
+      if (vg < lo) {
+        a = g;                 // gallop upward from the probe
+      } else {
+        const int g2 = g >> 1; // one halving step, then the binary search
+        const int r2 = h + g2 >= cap ? h + g2 - cap : h + g2;
+        const double v2 = e[r2];
+        if (v2 < lo) {
+          a = g2;
+          b = g;
+          vb = vg;
+        } else {
+          b = g2;
+          vb = v2;
+        }
+        goto search;           // bracketed: no gallop
+      }
+    }
     for (;;) {
       b = a + step;
       if (b >= c) {
@@ -402,6 +433,7 @@ AS_NOINL AS_HD EmWin em_window(const double* e, int h, int c, double first, doub
       a = b;
       step <<= 1;
     }
+  search:
     while (b - a > 1) {
       const int mid = (a + b) >> 1;
       const int rm = h + mid >= cap ? h + mid - cap : h + mid;
@@ -671,7 +703,8 @@ struct Sim {
   // dropped lazily (here, by binary search, and when the ring fills), which
   // is exact because query times never decrease.
   AS_HD bool interval(Inst& I, double now, double* out) {
-    const EmWin r = em_window(em(I.id), I.em_h, I.em_c, I.em_first, I.em_last, now - sc().window, (int)L.ecap);
+    const EmWin r = em_window<(IPL == 2)>(em(I.id), I.em_h, I.em_c, I.em_first, I.em_last, now - sc().window,
+                                          (int)L.ecap);
     I.em_h = r.h;
     I.em_c = r.c;
     I.em_first = r.first;
