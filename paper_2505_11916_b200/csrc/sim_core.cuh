@@ -571,6 +571,23 @@ struct Sim {
   // not at every push: a run that exhausts it ends as BUFFER_OVERFLOW.
   AS_HD uint32_t next_seq() { return u().seq++; }
 
+  // The 2^28 budget test on the per-step paths (lane 0).  The latency build
+  // (!COMPACT) uses a branch-free form (selects and plain stores: no call and
+  // no nested reconvergence region); the occupancy build keeps the call (the
+  // branch-free form cost C5 2.4 % through code layout).  First error wins
+  // either way, as in status_set().
+  AS_HD void seq_check(uint32_t seq) {
+    if (COMPACT) {
+      if (seq >= SEQ_LIMIT) set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_SEQ);
+    } else {
+      Uniform& U = u();
+      const bool over = seq >= SEQ_LIMIT && U.status == ARROW_OK;
+      const int st0 = U.status, ov0 = U.overflow;
+      U.status = over ? ARROW_BUFFER_OVERFLOW : st0;
+      U.overflow = over ? ARROW_OVF_SEQ : ov0;
+    }
+  }
+
   // ------------------------------------------------------ warp argmin --
 
   AS_HD int warp_argmin(uint64_t key, uint32_t tie, bool valid) {
@@ -703,7 +720,7 @@ struct Sim {
   // dropped lazily (here, by binary search, and when the ring fills), which
   // is exact because query times never decrease.
   AS_HD bool interval(Inst& I, double now, double* out) {
-    const EmWin r = em_window<(IPL == 2)>(em(I.id), I.em_h, I.em_c, I.em_first, I.em_last, now - sc().window,
+    const EmWin r = em_window<(IPL == 2 || !COMPACT)>(em(I.id), I.em_h, I.em_c, I.em_first, I.em_last, now - sc().window,
                                           (int)L.ecap);
     I.em_h = r.h;
     I.em_c = r.c;
@@ -1901,7 +1918,7 @@ struct Sim {
     w.sync();
     lane0([&] {
       Uniform& U = u();
-      if (base + total_push >= SEQ_LIMIT) set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_SEQ);
+      seq_check(base + total_push);
       U.seq = base + total_push;
       U.esp = 0;  // every quiet event emits a token
       U.n_events += total_part;
@@ -2438,7 +2455,7 @@ struct Sim {
     }
     lane0([&] {
       Uniform& U = u();
-      if (base + total_push >= SEQ_LIMIT) set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_SEQ);
+      seq_check(base + total_push);
       U.seq = base + total_push;
       U.esp = 0;
       U.n_events += packed & 0xffffu;
@@ -2594,7 +2611,7 @@ struct Sim {
       const int ev = h.code;
       now = tkey_inv(h.k);
       lane0([&] {
-        if (u().seq >= SEQ_LIMIT) set_status(ARROW_BUFFER_OVERFLOW, ARROW_OVF_SEQ);
+        seq_check(u().seq);
         u().now = now;
         u().esp++;
         u().n_events++;
